@@ -1,0 +1,88 @@
+"""In-tree build of every native artefact (sm_100a CUDA + C++ host + the test oracles).
+
+    python -m paper_2006_11972_b200.build          # everything that is out of date
+
+Outputs (git-ignored, but shipped to the GPU box by gpurun's snapshot):
+    paper_2006_11972_b200/libsmx.so               executor: CUDA kernels + C ABI (include/smx.h)
+    paper_2006_11972_b200/_stagemerge*.so         host library (C++ stagemerge API) + Python binding
+    oracle/liboracle.so                           CPU oracle (test infrastructure)
+    oracle/_ref/libstagemerge_ref.so              reference hpseq/plan, only when /root/reference exists
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = ROOT / "include"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NLOHMANN = Path(sysconfig.get_paths()["purelib"]) / "include/cudnn_frontend/thirdparty/nlohmann"
+
+CUDA_SOURCES = [CSRC / "smx.cu"]
+CUDA_DEPS = CUDA_SOURCES + sorted((CSRC / "kernels").glob("*.cuh")) + [INCLUDE / "smx.h"]
+HOST_SOURCES = sorted((CSRC / "host").glob("*.cpp"))
+HOST_DEPS = HOST_SOURCES + sorted((CSRC / "host").glob("*.hpp")) + sorted((INCLUDE / "stagemerge").glob("*.hpp"))
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, cwd=None):
+    print("+", " ".join(str(c) for c in cmd), flush=True)
+    subprocess.run([str(c) for c in cmd], check=True, cwd=cwd)
+
+
+def build_smx(force: bool = False) -> Path:
+    out = PKG / "libsmx.so"
+    if force or _stale(out, CUDA_DEPS):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xptxas", "-v,-warn-spills",
+              "-Xcompiler", "-fPIC,-Wall", "-shared", f"-I{INCLUDE}", "-o", out, *CUDA_SOURCES])
+    return out
+
+
+def host_ext_path() -> Path:
+    return PKG / ("_stagemerge" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force: bool = False) -> Path | None:
+    if not HOST_SOURCES:
+        return None
+    out = host_ext_path()
+    smx = PKG / "libsmx.so"
+    if force or _stale(out, HOST_DEPS + [smx]):
+        import pybind11
+
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-fvisibility=hidden",
+              f"-I{INCLUDE}", f"-I{CSRC / 'host'}", f"-I{NLOHMANN}", f"-I{pybind11.get_include()}",
+              f"-I{sysconfig.get_paths()['include']}", "-o", out, *HOST_SOURCES,
+              f"-L{PKG}", "-lsmx", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
+def build_oracle(force: bool = False) -> None:
+    args = ["make", "-C", ROOT / "oracle"]
+    if force:
+        args.append("-B")
+    _run(args)
+    if Path("/root/reference/proj/core/src/plan.cpp").exists():
+        _run(["make", "-C", ROOT / "oracle", "ref"] + (["-B"] if force else []))
+
+
+def build_all(force: bool = False) -> None:
+    build_smx(force)
+    build_host(force)
+    build_oracle(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

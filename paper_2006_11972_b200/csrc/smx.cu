@@ -1,0 +1,784 @@
+// smx.cu — the B200 stage executor behind include/smx.h.
+//
+// One smx_ctx owns one GPU: the slot slab (w | m per slot), the gradient slab, the checkpoint
+// pool (w | m per entry), the per-slot hp table and loss history, the synthetic dataset and
+// the activation scratch.  A lockstep trains every active slot by one step with one launch
+// per kernel class (grouped over slots); smx_train replays the lockstep sequence through a
+// CUDA graph keyed by the active slot set.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/smx.h"
+#include "kernels/common.cuh"
+#include "kernels/gemm_simt.cuh"
+#include "kernels/step_kernels.cuh"
+
+using namespace smx;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct SmxError {
+    int code;
+    std::string what;
+};
+
+[[noreturn]] void fail(int code, const std::string& what) { throw SmxError{code, what}; }
+
+void ck(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) fail(SMX_EDEVICE, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kEvalChunk = 16;  // slots evaluated per eval launch group
+
+}  // namespace
+
+struct smx_ctx {
+    smx_model_desc d{};
+    int device = 0;
+    int S = 0, C = 0;
+    cudaStream_t stream = nullptr;
+
+    float* slab = nullptr;      // S x 2 x PAlloc  (w | m)
+    float* grad = nullptr;      // S x PAlloc
+    float* pool = nullptr;      // C x 2 x PAlloc  (w | m)
+    SlotState* st = nullptr;    // S
+    SlotState* ck_st = nullptr; // C
+    float* hp = nullptr;        // S x cap x 4
+    float* loss = nullptr;      // S x cap
+    float* act = nullptr;       // S x kActStride
+    float* xtrain = nullptr;    // (n_train + max_batch) x 784
+    int* ytrain = nullptr;
+    float* xval = nullptr;      // n_val x 784
+    int* yval = nullptr;
+    float* eval_act = nullptr;  // kEvalChunk x n_val x (256 + 256 + 16)
+    float* eval_scratch = nullptr;
+    double* eval_out = nullptr;
+    int* eval_slots = nullptr;
+    CopyJob* jobs = nullptr;    // device job list for fork copies
+    int jobs_cap = 0;
+    std::vector<char> ck_valid;
+
+    struct Graph {
+        int* d_slots = nullptr;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::map<std::vector<int>, Graph> graphs;
+    int* scratch_slots = nullptr;  // for non-graph launches
+    bool use_graphs = true;
+    bool timing = false;
+    smx_stats stats{};
+    cudaEvent_t ev[8] = {};
+
+    long long slab_stride() const { return 2 * kPAlloc; }
+};
+
+namespace {
+
+void launch_check(smx_ctx* c, const char* what) {
+    c->stats.launches += 1;
+    ck(cudaGetLastError(), what);
+}
+
+StepCtx step_ctx(smx_ctx* c, const int* d_slots) {
+    return StepCtx{d_slots, c->st, c->hp, c->d.max_steps};
+}
+
+GemmArgs base_args(smx_ctx* c, const int* d_slots) {
+    GemmArgs a{};
+    a.slots = d_slots;
+    a.st = c->st;
+    a.hp = c->hp;
+    a.hp_cap = c->d.max_steps;
+    a.n_train_mask = c->d.n_train - 1;
+    return a;
+}
+
+template <int AM, int BMODE, int EPI>
+void gemm(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
+    dim3 grid((a.N + kTN - 1) / kTN, (m_max + kTM - 1) / kTM, groups);
+    gemm_simt_kernel<AM, BMODE, EPI><<<grid, 256, 0, c->stream>>>(a);
+    launch_check(c, "gemm_simt");
+}
+
+// One lockstep of the MLP over `n` slots listed in device array d_slots.
+void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
+    const int mb = c->d.max_batch;
+    const long long SW = c->slab_stride(), AS = kActStride;
+    float* W = c->slab;
+    float* G = c->grad;
+    float* A = c->act;
+    StepCtx sc = step_ctx(c, d_slots);
+
+    {
+        // ---- forward
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{c->xtrain, 0, kD0, 1};
+            g.b = Opnd{W + kOffW1, SW, kD0, 0};
+            g.c = A + kActH1; g.c_stride = AS; g.ldc = kH;
+            g.bias = W + kOffB1; g.bias_stride = SW;
+            g.M = mb; g.m_is_bs = 1; g.N = kH; g.K = kD0;
+            gemm<0, 0, kEpiBiasRelu>(c, g, n, mb);
+        }
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{A + kActH1, AS, kH, 0};
+            g.b = Opnd{W + kOffW2, SW, kH, 0};
+            g.c = A + kActH2; g.c_stride = AS; g.ldc = kH;
+            g.bias = W + kOffB2; g.bias_stride = SW;
+            g.M = mb; g.m_is_bs = 1; g.N = kH; g.K = kH;
+            gemm<0, 0, kEpiBiasRelu>(c, g, n, mb);
+        }
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{A + kActH2, AS, kH, 0};
+            g.b = Opnd{W + kOffW3, SW, kH, 0};
+            g.c = A + kActZ; g.c_stride = AS; g.ldc = kCP;
+            g.bias = W + kOffB3; g.bias_stride = SW;
+            g.M = mb; g.m_is_bs = 1; g.N = kCP; g.K = kH;
+            gemm<0, 0, kEpiBias>(c, g, n, mb);
+        }
+        // ---- loss
+        loss_train_kernel<<<n, kMaxBatch, 0, c->stream>>>(sc, c->ytrain, c->d.n_train - 1, A, AS, c->loss);
+        launch_check(c, "loss_train");
+        // ---- layer 3 grads
+        {
+            GemmArgs g = base_args(c, d_slots);  // gW3[c][k] = sum_r dZ[r][c] H2[r][k]
+            g.a = Opnd{A + kActDZ, AS, kCP, 0};
+            g.b = Opnd{A + kActH2, AS, kH, 0};
+            g.c = G + kOffW3; g.c_stride = kPAlloc; g.ldc = kH;
+            g.M = kCP; g.N = kH; g.K = mb; g.k_is_bs = 1;
+            gemm<1, 1, kEpiStore>(c, g, n, kCP);
+        }
+        colsum_kernel<<<dim3(1, n), 128, 0, c->stream>>>(sc, A, AS, kActDZ, kCP, kCP, G, kPAlloc, kOffB3);
+        launch_check(c, "colsum3");
+        {
+            GemmArgs g = base_args(c, d_slots);  // dH2[r][k] = (H2>0) sum_c dZ[r][c] W3[c][k]
+            g.a = Opnd{A + kActDZ, AS, kCP, 0};
+            g.b = Opnd{W + kOffW3, SW, kH, 0};
+            g.c = A + kActDH2; g.c_stride = AS; g.ldc = kH;
+            g.mask = A + kActH2; g.mask_stride = AS; g.ldmask = kH;
+            g.M = mb; g.m_is_bs = 1; g.N = kH; g.K = kCP;
+            gemm<0, 1, kEpiMask>(c, g, n, mb);
+        }
+        // ---- layer 2 grads
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{A + kActDH2, AS, kH, 0};
+            g.b = Opnd{A + kActH1, AS, kH, 0};
+            g.c = G + kOffW2; g.c_stride = kPAlloc; g.ldc = kH;
+            g.M = kH; g.N = kH; g.K = mb; g.k_is_bs = 1;
+            gemm<1, 1, kEpiStore>(c, g, n, kH);
+        }
+        colsum_kernel<<<dim3(2, n), 128, 0, c->stream>>>(sc, A, AS, kActDH2, kH, kH, G, kPAlloc, kOffB2);
+        launch_check(c, "colsum2");
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{A + kActDH2, AS, kH, 0};
+            g.b = Opnd{W + kOffW2, SW, kH, 0};
+            g.c = A + kActDH1; g.c_stride = AS; g.ldc = kH;
+            g.mask = A + kActH1; g.mask_stride = AS; g.ldmask = kH;
+            g.M = mb; g.m_is_bs = 1; g.N = kH; g.K = kH;
+            gemm<0, 1, kEpiMask>(c, g, n, mb);
+        }
+        // ---- layer 1 grads
+        {
+            GemmArgs g = base_args(c, d_slots);
+            g.a = Opnd{A + kActDH1, AS, kH, 0};
+            g.b = Opnd{c->xtrain, 0, kD0, 1};
+            g.c = G + kOffW1; g.c_stride = kPAlloc; g.ldc = kD0;
+            g.M = kH; g.N = kD0; g.K = mb; g.k_is_bs = 1;
+            gemm<1, 1, kEpiStore>(c, g, n, kH);
+        }
+        colsum_kernel<<<dim3(2, n), 128, 0, c->stream>>>(sc, A, AS, kActDH1, kH, kH, G, kPAlloc, kOffB1);
+        launch_check(c, "colsum1");
+    }
+    // ---- K5 update + advance
+    if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+    {
+        const long long n4 = kPAlloc / 4;
+        const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
+        sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, W, SW, G, kPAlloc, n4);
+        launch_check(c, "sgd_update");
+    }
+    if (c->timing) cudaEventRecord(c->ev[3], c->stream);
+    advance_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(sc, n);
+    launch_check(c, "advance");
+}
+
+void free_graphs(smx_ctx* c) {
+    for (auto& [k, g] : c->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.d_slots) cudaFree(g.d_slots);
+    }
+    c->graphs.clear();
+}
+
+smx_ctx::Graph& graph_for(smx_ctx* c, const std::vector<int>& slots) {
+    auto it = c->graphs.find(slots);
+    if (it != c->graphs.end()) return it->second;
+    if (c->graphs.size() >= 256) free_graphs(c);
+    smx_ctx::Graph g;
+    const int n = (int)slots.size();
+    ck(cudaMalloc(&g.d_slots, sizeof(int) * n), "cudaMalloc graph slots");
+    ck(cudaMemcpyAsync(g.d_slots, slots.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream),
+       "slots H2D");
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    const long long launches = c->stats.launches;
+    try {
+        enqueue_lockstep(c, g.d_slots, n);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        throw;
+    }
+    c->stats.launches = launches;
+    ck(cudaStreamEndCapture(c->stream, &graph), "end capture");
+    ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    return c->graphs.emplace(slots, g).first->second;
+}
+
+void gen_dataset(smx_ctx* c) {
+    const long long rows = (long long)c->d.n_train + c->d.max_batch;
+    gen_x_kernel<<<1184, 256, 0, c->stream>>>(c->xtrain, rows, c->d.n_train, c->d.seed, kStreamTrain);
+    launch_check(c, "gen_x train");
+    gen_labels_kernel<<<296, 128, 0, c->stream>>>(c->xtrain, c->ytrain, rows, c->d.seed);
+    launch_check(c, "gen_labels train");
+    gen_x_kernel<<<1184, 256, 0, c->stream>>>(c->xval, c->d.n_val, c->d.n_val, c->d.seed, kStreamVal);
+    launch_check(c, "gen_x val");
+    gen_labels_kernel<<<296, 128, 0, c->stream>>>(c->xval, c->yval, c->d.n_val, c->d.seed);
+    launch_check(c, "gen_labels val");
+}
+
+float init_scale(int fan_in) {
+    // bound = sqrt(6 / fan_in) rounded to fp32, then scaled by 2^-23 (exact)
+    return (float)std::sqrt(6.0 / (double)fan_in) * (1.0f / 8388608.0f);
+}
+
+void check_slot(smx_ctx* c, int slot) {
+    if (slot < 0 || slot >= c->S) fail(SMX_ECONFIG, "slot " + std::to_string(slot) + " out of range");
+}
+void check_ckpt(smx_ctx* c, int ck_) {
+    if (ck_ < 0 || ck_ >= c->C) fail(SMX_ECONFIG, "checkpoint " + std::to_string(ck_) + " out of range");
+}
+
+void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
+    if (jobs.empty()) return;
+    if ((int)jobs.size() > c->jobs_cap) {
+        if (c->jobs) cudaFree(c->jobs);
+        c->jobs_cap = (int)jobs.size() * 2;
+        ck(cudaMalloc(&c->jobs, sizeof(CopyJob) * c->jobs_cap), "cudaMalloc jobs");
+    }
+    ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * jobs.size(), cudaMemcpyHostToDevice, c->stream),
+       "jobs H2D");
+    const long long n4 = 2 * kPAlloc / 4;
+    if (c->timing) cudaEventRecord(c->ev[4], c->stream);
+    fork_copy_kernel<<<dim3(148, (unsigned)jobs.size()), 256, 0, c->stream>>>(c->jobs, n4);
+    launch_check(c, "fork_copy");
+    if (c->timing) {
+        cudaEventRecord(c->ev[5], c->stream);
+        cudaEventSynchronize(c->ev[5]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+        c->stats.fork_ms += ms;
+        c->stats.fork_launches += 1;
+    }
+    // the job list lives in device memory reused by the next copy: keep ordering simple
+    ck(cudaStreamSynchronize(c->stream), "fork sync");
+    c->stats.forks += (long long)jobs.size();
+}
+
+int guard(const std::function<void()>& f) {
+    try {
+        f();
+        return SMX_OK;
+    } catch (const SmxError& e) {
+        g_err = e.what;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SMX_EDEVICE;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* smx_last_error(void) { return g_err.c_str(); }
+const char* smx_version(void) { return "smx 0.1 (sm_100a; exact SIMT + tcgen05 3xTF32)"; }
+
+int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, smx_ctx** out) {
+    return guard([&] {
+        if (!desc || !out) fail(SMX_ECONFIG, "null argument");
+        const smx_model_desc& d = *desc;
+        if (d.model != SMX_MODEL_MLP) fail(SMX_ECONFIG, "unsupported model id " + std::to_string(d.model));
+        if (d.max_batch < 1 || d.max_batch > kMaxBatch) fail(SMX_ECONFIG, "max_batch must be in [1, 256]");
+        if (d.n_train < 256 || (d.n_train & (d.n_train - 1))) fail(SMX_ECONFIG, "n_train must be a power of two >= 256");
+        if (d.n_val < 128 || d.n_val % 128) fail(SMX_ECONFIG, "n_val must be a positive multiple of 128");
+        if (d.max_steps < 1) fail(SMX_ECONFIG, "max_steps must be >= 1");
+        if (d.gemm_mode != SMX_GEMM_EXACT) fail(SMX_ECONFIG, "gemm_mode not available in this build");
+        if (n_slots < 1 || n_ckpts < 0) fail(SMX_ECONFIG, "bad slot/checkpoint counts");
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) fail(SMX_ECONFIG, "device out of range");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        auto* c = new smx_ctx();
+        c->d = d;
+        c->device = device;
+        c->S = n_slots;
+        c->C = n_ckpts;
+        try {
+            ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+            const long long P2 = 2 * kPAlloc;
+            ck(cudaMalloc(&c->slab, sizeof(float) * P2 * n_slots), "slab");
+            ck(cudaMalloc(&c->grad, sizeof(float) * kPAlloc * n_slots), "grad");
+            if (n_ckpts) ck(cudaMalloc(&c->pool, sizeof(float) * P2 * n_ckpts), "pool");
+            ck(cudaMalloc(&c->st, sizeof(SlotState) * n_slots), "state");
+            ck(cudaMalloc(&c->ck_st, sizeof(SlotState) * (n_ckpts ? n_ckpts : 1)), "ck state");
+            ck(cudaMalloc(&c->hp, sizeof(float) * 4 * (long long)d.max_steps * n_slots), "hp");
+            ck(cudaMalloc(&c->loss, sizeof(float) * (long long)d.max_steps * n_slots), "loss");
+            ck(cudaMalloc(&c->act, sizeof(float) * kActStride * n_slots), "act");
+            const long long rows = (long long)d.n_train + d.max_batch;
+            ck(cudaMalloc(&c->xtrain, sizeof(float) * rows * kD0), "xtrain");
+            ck(cudaMalloc(&c->ytrain, sizeof(int) * rows), "ytrain");
+            ck(cudaMalloc(&c->xval, sizeof(float) * (long long)d.n_val * kD0), "xval");
+            ck(cudaMalloc(&c->yval, sizeof(int) * d.n_val), "yval");
+            ck(cudaMalloc(&c->eval_act, sizeof(float) * kEvalChunk * (long long)d.n_val * (2 * kH + kCP)), "eval act");
+            ck(cudaMalloc(&c->eval_scratch, sizeof(float) * kEvalChunk * (long long)d.n_val), "eval scratch");
+            ck(cudaMalloc(&c->eval_out, sizeof(double) * 2 * kEvalChunk), "eval out");
+            ck(cudaMalloc(&c->eval_slots, sizeof(int) * kEvalChunk), "eval slots");
+            ck(cudaMalloc(&c->scratch_slots, sizeof(int) * n_slots), "scratch slots");
+            ck(cudaMemsetAsync(c->grad, 0, sizeof(float) * kPAlloc * n_slots, c->stream), "grad zero");
+            ck(cudaMemsetAsync(c->hp, 0, sizeof(float) * 4 * (long long)d.max_steps * n_slots, c->stream), "hp zero");
+            ck(cudaMemsetAsync(c->loss, 0, sizeof(float) * (long long)d.max_steps * n_slots, c->stream), "loss zero");
+            ck(cudaMemsetAsync(c->act, 0, sizeof(float) * kActStride * n_slots, c->stream), "act zero");
+            ck(cudaMemsetAsync(c->st, 0, sizeof(SlotState) * n_slots, c->stream), "state zero");
+            for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
+            c->ck_valid.assign(n_ckpts, 0);
+            gen_dataset(c);
+            ck(cudaStreamSynchronize(c->stream), "open sync");
+        } catch (...) {
+            smx_close(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int smx_close(smx_ctx* c) {
+    if (!c) return SMX_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    free_graphs(c);
+    void* bufs[] = {c->slab, c->grad, c->pool, c->st, c->ck_st, c->hp, c->loss, c->act, c->xtrain, c->ytrain,
+                    c->xval, c->yval, c->eval_act, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
+                    c->scratch_slots};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return SMX_OK;
+}
+
+int smx_param_count(const smx_ctx* c, int64_t* p, int64_t* p_alloc) {
+    (void)c;
+    if (p) *p = kPAlgo;
+    if (p_alloc) *p_alloc = kPAlloc;
+    return SMX_OK;
+}
+
+int smx_dataset_digest(smx_ctx* c, uint64_t* out) {
+    return guard([&] {
+        cudaSetDevice(c->device);
+        const long long rows = (long long)c->d.n_train + c->d.max_batch;
+        std::vector<float> x(rows * kD0);
+        std::vector<int> y(rows);
+        std::vector<float> vx((long long)c->d.n_val * kD0);
+        std::vector<int> vy(c->d.n_val);
+        ck(cudaMemcpyAsync(x.data(), c->xtrain, sizeof(float) * x.size(), cudaMemcpyDeviceToHost, c->stream), "x D2H");
+        ck(cudaMemcpyAsync(y.data(), c->ytrain, sizeof(int) * y.size(), cudaMemcpyDeviceToHost, c->stream), "y D2H");
+        ck(cudaMemcpyAsync(vx.data(), c->xval, sizeof(float) * vx.size(), cudaMemcpyDeviceToHost, c->stream), "vx D2H");
+        ck(cudaMemcpyAsync(vy.data(), c->yval, sizeof(int) * vy.size(), cudaMemcpyDeviceToHost, c->stream), "vy D2H");
+        ck(cudaStreamSynchronize(c->stream), "digest sync");
+        uint64_t h = 0xcbf29ce484222325ull;
+        auto eat = [&](const void* p, size_t n) {
+            const unsigned char* b = static_cast<const unsigned char*>(p);
+            for (size_t i = 0; i < n; ++i) {
+                h ^= b[i];
+                h *= 0x100000001b3ull;
+            }
+        };
+        eat(x.data(), x.size() * 4);
+        eat(y.data(), y.size() * 4);
+        eat(vx.data(), vx.size() * 4);
+        eat(vy.data(), vy.size() * 4);
+        *out = h;
+    });
+}
+
+int smx_hp_upload(smx_ctx* c, int slot, int64_t step0, int64_t n, const float* hp) {
+    return guard([&] {
+        check_slot(c, slot);
+        if (step0 < 0 || n < 0 || step0 + n > c->d.max_steps)
+            fail(SMX_ECONFIG, "hp rows [" + std::to_string(step0) + ", " + std::to_string(step0 + n) +
+                                  ") exceed max_steps " + std::to_string(c->d.max_steps));
+        for (int64_t i = 0; i < n; ++i) {
+            const float bs = hp[i * 4 + 3];
+            if (!(bs >= 1.0f) || bs > (float)c->d.max_batch || bs != std::floor(bs))
+                fail(SMX_ECONFIG, "batch size " + std::to_string(bs) + " at step " + std::to_string(step0 + i) +
+                                      " outside [1, max_batch]");
+        }
+        if (n == 0) return;
+        cudaSetDevice(c->device);
+        // pageable source: cudaMemcpyAsync stages it, so the caller's buffer is free on return
+        ck(cudaMemcpyAsync(c->hp + ((long long)slot * c->d.max_steps + step0) * 4, hp, sizeof(float) * 4 * n,
+                           cudaMemcpyHostToDevice, c->stream),
+           "hp H2D");
+    });
+}
+
+int smx_slot_init(smx_ctx* c, int slot) {
+    return guard([&] {
+        check_slot(c, slot);
+        cudaSetDevice(c->device);
+        float* w = c->slab + c->slab_stride() * slot;
+        init_kernel<<<296, 256, 0, c->stream>>>(w, w + kPAlloc, c->d.seed, init_scale(kD0), init_scale(kH),
+                                                init_scale(kH));
+        launch_check(c, "init");
+        ck(cudaMemsetAsync(c->st + slot, 0, sizeof(SlotState), c->stream), "state reset");
+    });
+}
+
+int smx_slot_load(smx_ctx* c, int slot, int ckpt) {
+    return guard([&] {
+        check_slot(c, slot);
+        check_ckpt(c, ckpt);
+        if (!c->ck_valid[ckpt]) fail(SMX_EINTEGRITY, "load from empty checkpoint entry " + std::to_string(ckpt));
+        cudaSetDevice(c->device);
+        CopyJob j{reinterpret_cast<const float4*>(c->pool + c->slab_stride() * ckpt),
+                  reinterpret_cast<float4*>(c->slab + c->slab_stride() * slot), c->ck_st + ckpt, c->st + slot};
+        run_copy(c, {j});
+    });
+}
+
+int smx_slot_save(smx_ctx* c, int slot, int ckpt) {
+    return guard([&] {
+        check_slot(c, slot);
+        check_ckpt(c, ckpt);
+        cudaSetDevice(c->device);
+        CopyJob j{reinterpret_cast<const float4*>(c->slab + c->slab_stride() * slot),
+                  reinterpret_cast<float4*>(c->pool + c->slab_stride() * ckpt), c->st + slot, c->ck_st + ckpt};
+        run_copy(c, {j});
+        c->ck_valid[ckpt] = 1;
+    });
+}
+
+int smx_ckpt_free(smx_ctx* c, int ckpt) {
+    return guard([&] {
+        check_ckpt(c, ckpt);
+        c->ck_valid[ckpt] = 0;
+    });
+}
+
+int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
+    return guard([&] {
+        check_ckpt(dst, dst_ckpt);
+        check_ckpt(src, src_ckpt);
+        if (!src->ck_valid[src_ckpt]) fail(SMX_EINTEGRITY, "peer copy from empty checkpoint entry");
+        ck(cudaStreamSynchronize(src->stream), "src sync");
+        cudaSetDevice(dst->device);
+        const size_t bytes = sizeof(float) * dst->slab_stride();
+        if (dst->device != src->device) {
+            int can = 0;
+            ck(cudaDeviceCanAccessPeer(&can, dst->device, src->device), "can access peer");
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
+                cudaGetLastError();
+            }
+        }
+        if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
+        ck(cudaMemcpyPeerAsync(dst->pool + dst->slab_stride() * dst_ckpt, dst->device,
+                               src->pool + src->slab_stride() * src_ckpt, src->device, bytes, dst->stream),
+           "peer copy");
+        ck(cudaMemcpyPeerAsync(dst->ck_st + dst_ckpt, dst->device, src->ck_st + src_ckpt, src->device,
+                               sizeof(SlotState), dst->stream),
+           "peer state copy");
+        if (dst->timing) {
+            cudaEventRecord(dst->ev[5], dst->stream);
+            cudaEventSynchronize(dst->ev[5]);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, dst->ev[4], dst->ev[5]);
+            dst->stats.fork_ms += ms;
+            dst->stats.fork_launches += 1;
+        }
+        ck(cudaStreamSynchronize(dst->stream), "peer sync");
+        dst->ck_valid[dst_ckpt] = 1;
+        dst->stats.forks += 1;
+    });
+}
+
+int smx_slot_state(smx_ctx* c, int slot, int64_t* step, int64_t* offset) {
+    return guard([&] {
+        check_slot(c, slot);
+        cudaSetDevice(c->device);
+        SlotState s;
+        ck(cudaMemcpyAsync(&s, c->st + slot, sizeof s, cudaMemcpyDeviceToHost, c->stream), "state D2H");
+        ck(cudaStreamSynchronize(c->stream), "state sync");
+        if (step) *step = s.step;
+        if (offset) *offset = s.offset;
+    });
+}
+
+int smx_slot_read(smx_ctx* c, int slot, float* w, float* m) {
+    return guard([&] {
+        check_slot(c, slot);
+        cudaSetDevice(c->device);
+        const float* base = c->slab + c->slab_stride() * slot;
+        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
+        if (m) ck(cudaMemcpyAsync(m, base + kPAlloc, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
+        ck(cudaStreamSynchronize(c->stream), "read sync");
+    });
+}
+
+int smx_slot_write(smx_ctx* c, int slot, const float* w, const float* m, int64_t step, int64_t offset) {
+    return guard([&] {
+        check_slot(c, slot);
+        cudaSetDevice(c->device);
+        float* base = c->slab + c->slab_stride() * slot;
+        ck(cudaMemcpyAsync(base, w, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
+        ck(cudaMemcpyAsync(base + kPAlloc, m, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
+        SlotState s{step, offset};
+        ck(cudaMemcpyAsync(c->st + slot, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state H2D");
+        ck(cudaStreamSynchronize(c->stream), "write sync");
+    });
+}
+
+int smx_ckpt_read(smx_ctx* c, int ckpt, float* w, float* m, int64_t* step, int64_t* offset) {
+    return guard([&] {
+        check_ckpt(c, ckpt);
+        if (!c->ck_valid[ckpt]) fail(SMX_EINTEGRITY, "read of empty checkpoint entry");
+        cudaSetDevice(c->device);
+        const float* base = c->pool + c->slab_stride() * ckpt;
+        SlotState s;
+        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
+        if (m) ck(cudaMemcpyAsync(m, base + kPAlloc, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
+        ck(cudaMemcpyAsync(&s, c->ck_st + ckpt, sizeof s, cudaMemcpyDeviceToHost, c->stream), "state D2H");
+        ck(cudaStreamSynchronize(c->stream), "ckpt read sync");
+        if (step) *step = s.step;
+        if (offset) *offset = s.offset;
+    });
+}
+
+int smx_ckpt_write(smx_ctx* c, int ckpt, const float* w, const float* m, int64_t step, int64_t offset) {
+    return guard([&] {
+        check_ckpt(c, ckpt);
+        cudaSetDevice(c->device);
+        float* base = c->pool + c->slab_stride() * ckpt;
+        ck(cudaMemcpyAsync(base, w, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
+        ck(cudaMemcpyAsync(base + kPAlloc, m, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
+        SlotState s{step, offset};
+        ck(cudaMemcpyAsync(c->ck_st + ckpt, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state H2D");
+        ck(cudaStreamSynchronize(c->stream), "ckpt write sync");
+        c->ck_valid[ckpt] = 1;
+    });
+}
+
+int smx_train(smx_ctx* c, int n_active, const int* slots, int n_steps) {
+    return guard([&] {
+        if (n_active < 0 || n_steps < 0) fail(SMX_ECONFIG, "negative counts");
+        if (n_active == 0 || n_steps == 0) return;
+        std::vector<int> v(slots, slots + n_active);
+        std::vector<char> seen(c->S, 0);
+        for (int s : v) {
+            check_slot(c, s);
+            if (seen[s]) fail(SMX_ECONFIG, "slot " + std::to_string(s) + " listed twice");
+            seen[s] = 1;
+        }
+        cudaSetDevice(c->device);
+        if (c->timing) {
+            // timing mode: plain launches bracketed by events (no graphs)
+            ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n_active, cudaMemcpyHostToDevice, c->stream),
+               "slots H2D");
+            for (int i = 0; i < n_steps; ++i) {
+                cudaEventRecord(c->ev[0], c->stream);
+                enqueue_lockstep(c, c->scratch_slots, n_active);
+                cudaEventRecord(c->ev[1], c->stream);
+                ck(cudaEventSynchronize(c->ev[1]), "timing sync");
+                float ms = 0, ums = 0;
+                cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+                cudaEventElapsedTime(&ums, c->ev[2], c->ev[3]);
+                c->stats.lockstep_ms += ms;
+                c->stats.update_ms += ums;
+                c->stats.update_launches += 1;
+                c->stats.gemm_ms += (ms - ums);
+                c->stats.gemm_launches += 1;
+            }
+        } else if (c->use_graphs && n_steps >= 2) {
+            smx_ctx::Graph& g = graph_for(c, v);
+            for (int i = 0; i < n_steps; ++i) {
+                ck(cudaGraphLaunch(g.exec, c->stream), "graph launch");
+                c->stats.launches += 14;
+            }
+        } else {
+            ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n_active, cudaMemcpyHostToDevice, c->stream),
+               "slots H2D");
+            for (int i = 0; i < n_steps; ++i) enqueue_lockstep(c, c->scratch_slots, n_active);
+            // scratch_slots is reused by the next call: make the H2D ordering explicit
+        }
+        c->stats.locksteps += n_steps;
+        c->stats.stage_steps += (long long)n_steps * n_active;
+    });
+}
+
+int smx_eval(smx_ctx* c, int n, const int* slots, double* out) {
+    return guard([&] {
+        cudaSetDevice(c->device);
+        const int nv = c->d.n_val;
+        const long long per = (long long)nv * (2 * kH + kCP);
+        for (int base = 0; base < n; base += kEvalChunk) {
+            const int k = std::min(kEvalChunk, n - base);
+            for (int i = 0; i < k; ++i) check_slot(c, slots[base + i]);
+            ck(cudaMemcpyAsync(c->eval_slots, slots + base, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream),
+               "eval slots H2D");
+            // Activations are addressed by position in the chunk, weights by slot id: each slot
+            // runs its three forward GEMMs as a one-group launch (M = n_val fills the GPU).
+            float* H1 = c->eval_act;
+            float* H2 = c->eval_act + (long long)nv * kH;
+            float* Z = c->eval_act + 2LL * nv * kH;
+            const long long SW = c->slab_stride();
+            for (int i = 0; i < k; ++i) {
+                int* d_one = c->eval_slots + i;
+                GemmArgs g = base_args(c, d_one);
+                g.a = Opnd{c->xval, 0, kD0, 0};
+                g.b = Opnd{c->slab + kOffW1, SW, kD0, 0};
+                g.c = H1 + per * i; g.c_stride = 0; g.ldc = kH;
+                g.bias = c->slab + kOffB1; g.bias_stride = SW;
+                g.M = nv; g.N = kH; g.K = kD0;
+                gemm<0, 0, kEpiBiasRelu>(c, g, 1, nv);
+                GemmArgs g2 = base_args(c, d_one);
+                g2.a = Opnd{H1 + per * i, 0, kH, 0};
+                g2.b = Opnd{c->slab + kOffW2, SW, kH, 0};
+                g2.c = H2 + per * i; g2.c_stride = 0; g2.ldc = kH;
+                g2.bias = c->slab + kOffB2; g2.bias_stride = SW;
+                g2.M = nv; g2.N = kH; g2.K = kH;
+                gemm<0, 0, kEpiBiasRelu>(c, g2, 1, nv);
+                GemmArgs g3 = base_args(c, d_one);
+                g3.a = Opnd{H2 + per * i, 0, kH, 0};
+                g3.b = Opnd{c->slab + kOffW3, SW, kH, 0};
+                g3.c = Z + per * i; g3.c_stride = 0; g3.ldc = kCP;
+                g3.bias = c->slab + kOffB3; g3.bias_stride = SW;
+                g3.M = nv; g3.N = kCP; g3.K = kH;
+                gemm<0, 0, kEpiBias>(c, g3, 1, nv);
+            }
+            eval_reduce_kernel<<<k, 256, 0, c->stream>>>(c->eval_slots, Z, per, c->yval, nv, c->eval_scratch,
+                                                         c->eval_out);
+            launch_check(c, "eval_reduce");
+            ck(cudaMemcpyAsync(out + 2LL * base, c->eval_out, sizeof(double) * 2 * k, cudaMemcpyDeviceToHost,
+                               c->stream),
+               "eval D2H");
+            ck(cudaStreamSynchronize(c->stream), "eval sync");
+        }
+    });
+}
+
+int smx_losses(smx_ctx* c, int slot, int64_t step0, int64_t n, float* out) {
+    return guard([&] {
+        check_slot(c, slot);
+        if (step0 < 0 || n < 0 || step0 + n > c->d.max_steps) fail(SMX_ECONFIG, "loss range out of bounds");
+        cudaSetDevice(c->device);
+        ck(cudaMemcpyAsync(out, c->loss + (long long)slot * c->d.max_steps + step0, sizeof(float) * n,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "loss D2H");
+        ck(cudaStreamSynchronize(c->stream), "loss sync");
+    });
+}
+
+int smx_sync(smx_ctx* c) {
+    return guard([&] {
+        cudaSetDevice(c->device);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int smx_set_timing(smx_ctx* c, int enabled) {
+    c->timing = enabled != 0;
+    return SMX_OK;
+}
+
+int smx_set_graphs(smx_ctx* c, int enabled) {
+    c->use_graphs = enabled != 0;
+    return SMX_OK;
+}
+
+int smx_get_stats(smx_ctx* c, smx_stats* out) {
+    *out = c->stats;
+    return SMX_OK;
+}
+
+int smx_reset_stats(smx_ctx* c) {
+    c->stats = smx_stats{};
+    return SMX_OK;
+}
+
+int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launch) {
+    return guard([&] {
+        cudaSetDevice(c->device);
+        if (n < 1 || reps < 1) fail(SMX_ECONFIG, "bad bench args");
+        if (kind == 0) {
+            if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
+            std::vector<int> v(n);
+            for (int i = 0; i < n; ++i) v[i] = i;
+            ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+            StepCtx sc = step_ctx(c, c->scratch_slots);
+            const long long n4 = kPAlloc / 4;
+            const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
+            for (int w = 0; w < 3; ++w)
+                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, kPAlloc, n4);
+            cudaEventRecord(c->ev[6], c->stream);
+            for (int r = 0; r < reps; ++r)
+                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, kPAlloc, n4);
+            cudaEventRecord(c->ev[7], c->stream);
+        } else if (kind == 1) {
+            if (n > c->C || n > c->S) fail(SMX_ECONFIG, "more checkpoints than allocated");
+            std::vector<CopyJob> jobs(n);
+            for (int i = 0; i < n; ++i)
+                jobs[i] = CopyJob{reinterpret_cast<const float4*>(c->slab + c->slab_stride() * i),
+                                  reinterpret_cast<float4*>(c->pool + c->slab_stride() * i), c->st + i, c->ck_st + i};
+            if (n > c->jobs_cap) {
+                if (c->jobs) cudaFree(c->jobs);
+                c->jobs_cap = n * 2;
+                ck(cudaMalloc(&c->jobs, sizeof(CopyJob) * c->jobs_cap), "jobs");
+            }
+            ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+            const long long n4 = 2 * kPAlloc / 4;
+            for (int w = 0; w < 3; ++w) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
+            cudaEventRecord(c->ev[6], c->stream);
+            for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
+            cudaEventRecord(c->ev[7], c->stream);
+        } else {
+            fail(SMX_ECONFIG, "unknown kernel kind");
+        }
+        ck(cudaGetLastError(), "bench launch");
+        ck(cudaEventSynchronize(c->ev[7]), "bench sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
+        *ms_per_launch = ms / reps;
+    });
+}
+
+}  // extern "C"
