@@ -62,7 +62,7 @@ def build_host(force: bool = False) -> Path | None:
     if force or _stale(out, HOST_DEPS + [smx]):
         import pybind11
 
-        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-fvisibility=hidden",
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall", "-Wextra", "-fvisibility=hidden",
               f"-I{INCLUDE}", f"-I{CSRC / 'host'}", f"-I{NLOHMANN}", f"-I{pybind11.get_include()}",
               f"-I{sysconfig.get_paths()['include']}", "-o", out, *HOST_SOURCES,
               f"-L{PKG}", "-lsmx", "-Wl,-rpath,$ORIGIN"])
