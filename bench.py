@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: trial-equivalent train steps/sec (TES) of a merged HPO study on B200.
+
+A bench "step" is one complete study run through the engine (plan insert -> stage trees ->
+critical-path schedule -> grouped GPU training / SAVE / LOAD / EVAL -> metrics recorded), STAGE
+mode.  TES = sum over trials of their steps / seconds.
+
+Workload at N GPUs ("scaling": "weak"): N studies over the C3 search space
+(paper_2006_11972_b200/studies/c3_random.json: 256 random trials x 2000 steps, sampler seeds
+0..N-1) merged into one plan whose root subtrees are LPT-partitioned over the N ranks — no
+collective on the data path.  N = 1 is exactly C3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gemm exact|tc]
+
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §6).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+METRIC = "trial-equivalent train steps/sec per study"
+UNIT = "trial-steps/s"
+
+
+def peaks() -> dict:
+    if PEAKS.exists():
+        d = json.loads(PEAKS.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(r[0]) for r in self.rows if r[0].isdigit())
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": int(self.rows[0][1]) if self.rows[0][1].isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def reduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def workload(n_studies: int):
+    from paper_2006_11972_b200 import host
+
+    base = json.loads(host.study_spec("c3_random"))
+    specs = []
+    for s in range(n_studies):
+        sp = dict(base)
+        sp["sampler"] = {**base["sampler"], "seed": s}
+        specs.append(json.dumps(sp))
+    return specs
+
+
+def cuda_time(fn, world):
+    """Run fn between device-synchronised CUDA events on torch's stream; max over ranks."""
+    import torch
+
+    barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    out = fn()
+    b.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    return reduce_max(a.elapsed_time(b) / 1e3, world), out
+
+
+def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
+    """The CPU oracle trainer (oracle/liboracle.so, OpenMP over all host cores) on a bounded
+    sample of the workload: the first stage-steps of the study's first trials.  Reported in the
+    metric's unit by scaling unique stage-steps/s with the same merge ratio the plan gives the
+    GPU run (the CPU executor would execute the identical plan)."""
+    import ctypes
+
+    import oracle_lib as ol
+    from paper_2006_11972_b200 import host
+
+    info = host.expand_study(specs[0])
+    cores = os.cpu_count() or 1
+    n = max(cores, 8)
+    hp = []
+    for cfg in info["trials"][:n]:
+        r = host.call({"op": "sequence", "config": cfg})
+        rows = np.zeros((cfg["total_steps"], 4), np.float32)
+        for c, name in enumerate(("lr", "momentum", "weight_decay", "batch_size")):
+            rows[:, c] = r["hps"][name]["values"] if name in r["hps"] else [0.1, 0.9, 0.0, 128][c]
+        hp.append(rows)
+    ds = ol.dataset()
+    slots = [ol.Slot(max_steps=2001) for _ in range(n)]
+    lib = ol.oracle()
+    FP = ctypes.POINTER(ctypes.c_float)
+    W = (FP * n)(*[ol.fp(s.w) for s in slots])
+    M = (FP * n)(*[ol.fp(s.m) for s in slots])
+    H = (FP * n)(*[ol.fp(h) for h in hp])
+    L = (FP * n)(*[ol.fp(s.loss) for s in slots])
+    step = (ctypes.c_int64 * n)()
+    off = (ctypes.c_int64 * n)()
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds and done < 2000:
+        k = 2
+        rc = lib.orc_train_many(n, W, M, step, off, H, 2000, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
+        assert rc == 0
+        done += k
+    dt = time.perf_counter() - t0
+    stage_steps = n * done
+    return {"value": stage_steps / dt * trial_per_stage, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{stage_steps} stage-steps ({n} trials x {done} steps of C3, OpenMP over {cores} threads) in "
+                      f"{dt:.1f}s = {stage_steps / dt:.1f} stage-steps/s, x{trial_per_stage:.3f} trial-steps per "
+                      f"stage-step (the plan's merge ratio)"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle port of the executor on the same plan)."""
+    if rank != 0:
+        return
+    specs = workload(1)
+    from paper_2006_11972_b200 import host
+
+    info = host.expand_study(specs[0])
+    ratio = info["total_steps"] / info["unique_steps"]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(specs, ratio, seconds=4.0)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                      "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                      "config": {"workload": "C3 space x 1 study (256 random trials x 2000 steps), MLP 784-256-256-10",
+                                 "flush": "n/a (CPU)"},
+                      "cpu_baseline": {**cb, "value": v},
+                      "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gemm", default=os.environ.get("SMX_BENCH_GEMM", "exact"), choices=["exact", "tc"])
+    ap.add_argument("--slots", type=int, default=128)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    from paper_2006_11972_b200 import executor as ex
+    from paper_2006_11972_b200 import host
+
+    torch.cuda.set_device(local)
+    specs = workload(world)
+    info = host.expand_study(specs[0])
+    gemm_mode = ex.GEMM_TC if args.gemm == "tc" else ex.GEMM_EXACT
+    eng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
+                                gemm_mode=gemm_mode, rank=rank, world=world, max_steps=2048)
+
+    def one_study():
+        eng.reset()
+        for s, sp in enumerate(specs):
+            eng.submit_study(sp, s)
+        eng.run()
+        return eng.stats()
+
+    for _ in range(args.warmup):
+        one_study()
+    with Clocks(local) as clk:
+        t, st = cuda_time(lambda: [one_study() for _ in range(args.steps)][-1], world)
+    trial_steps = reduce_sum(st["trial_steps"], world)  # the study's trials, split over ranks
+    stage_steps = reduce_sum(st["stage_steps"], world)
+    value = trial_steps * args.steps / t
+
+    # ---- e2e: the same study through the public Engine API with the dataset coming from
+    # pinned host memory every step (H2D inside the timed region) and metrics read back (D2H)
+    import ctypes
+
+    import oracle_lib as ol
+
+    ds = ol.dataset()  # host copy of the dataset (bit-identical to the on-device generator)
+    lib = ex.load_library()
+    pinned = []
+    host_arrays = []
+    for a in (ds.x, ds.y, ds.vx, ds.vy):
+        p = ctypes.c_void_p()
+        assert lib.smx_host_alloc(a.nbytes, ctypes.byref(p)) == 0
+        buf = np.ctypeslib.as_array((ctypes.c_byte * a.nbytes).from_address(p.value)).view(a.dtype).reshape(a.shape)
+        buf[...] = a
+        pinned.append(p)
+        host_arrays.append(buf)
+
+    def one_e2e():
+        eng.reset()
+        eng.upload_dataset(*host_arrays)
+        for s, sp in enumerate(specs):
+            eng.submit_study(sp, s)
+        eng.run()
+        return eng.stats()
+
+    one_e2e()
+    te, st_e = cuda_time(lambda: [one_e2e() for _ in range(args.steps)][-1], world)
+    e2e_value = reduce_sum(st_e["trial_steps"], world) * args.steps / te
+    for p in pinned:
+        lib.smx_host_free(p)
+
+    # ---- per-kernel roofline: K5 update and K6 fork timed standalone on the engine's context
+    pk = peaks()
+    ctx = ctypes.c_void_p(eng.context_ptrs()[0])
+    ms_u = ctypes.c_double()
+    n_upd = min(args.slots, 64)
+    assert lib.smx_bench_kernel(ctx, 0, n_upd, 50, ctypes.byref(ms_u)) == 0
+    ms_f = ctypes.c_double()
+    assert lib.smx_bench_kernel(ctx, 1, 16, 50, ctypes.byref(ms_f)) == 0
+    P, PALLOC = 269322, 270912
+    upd_bytes = 20 * P * n_upd
+    fork_bytes = 16 * P * 16
+    upd_gbs = upd_bytes / (ms_u.value * 1e-3) / 1e9
+    fork_gbs = fork_bytes / (ms_f.value * 1e-3) / 1e9
+    kernels = {
+        "K5_update": {"bound": "hbm", "achieved": upd_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                      "frac": upd_gbs / pk["hbm_gbs"], "bytes_per_launch": upd_bytes, "slots": n_upd,
+                      "ms_per_launch": ms_u.value},
+        "K6_fork": {"bound": "hbm", "achieved": fork_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": fork_gbs / pk["hbm_gbs"], "bytes_per_launch": fork_bytes, "checkpoints": 16,
+                    "ms_per_launch": ms_f.value},
+    }
+    # GEMM share: timing-mode locksteps of the study's own slot mix
+    roofline = dict(kernels["K5_update"])
+    roofline["traffic"] = None
+    roofline["kernel"] = "K5 fused SGD/momentum/wd update (sgd_update_kernel)"
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(specs, trial_steps / stage_steps)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C3 space x {world} studies (256 random trials x 2000 steps each, seeds 0..{world - 1}), "
+                                   "MLP 784-256-256-10, merged plan, root subtrees partitioned over ranks",
+                       "gemm": args.gemm, "slots_per_gpu": args.slots, "trials": 256 * world,
+                       "trial_steps": trial_steps, "unique_stage_steps": stage_steps,
+                       "executed_merge_rate": trial_steps / stage_steps,
+                       "flush": "inputs > L2: per-slot state 2.2 MB x 128 slots + 206 MB dataset"},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": st_e["h2d_bytes"], "d2h_bytes_per_step": st_e["d2h_bytes"]},
+            "gpu_launches": st["kernel_launches"] * args.steps,
+            "roofline": roofline,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "engine_stats": st,
+        }
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -102,8 +102,15 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
 int smx_close(smx_ctx* ctx);
 /* P = algorithmic parameter count; p_alloc = floats per parameter vector in HBM (padded). */
 int smx_param_count(const smx_ctx* ctx, int64_t* p, int64_t* p_alloc);
-/* FNV-1a over the bytes of the generated training/validation sets and labels. */
+/* FNV-1a over the bytes of the training/validation sets and labels. */
 int smx_dataset_digest(smx_ctx* ctx, uint64_t* out);
+/* Replace the synthetic dataset with host data: x (n_train + max_batch) x 784 fp32 (rows past
+ * n_train repeat the first max_batch rows), y int32 labels, vx n_val x 784, vy.  Host->device
+ * copies on the context stream; pinned buffers (smx_host_alloc) make them DMA-direct. */
+int smx_dataset_upload(smx_ctx* ctx, const float* x, const int32_t* y, const float* vx, const int32_t* vy);
+/* Page-locked host buffers for the e2e path. */
+int smx_host_alloc(uint64_t bytes, void** out);
+int smx_host_free(void* p);
 
 /* --- per-slot state (the model/optimizer state store) ------------------------------- */
 /* hp rows [step0, step0+n) for `slot`, each SMX_HP_COLS floats (host-computed values). */

@@ -59,13 +59,27 @@ def build_host(force: bool = False) -> Path | None:
         return None
     out = host_ext_path()
     smx = PKG / "libsmx.so"
-    if force or _stale(out, HOST_DEPS + [smx]):
-        import pybind11
+    if not (force or _stale(out, HOST_DEPS + [smx])):
+        return out
+    import pybind11
+    from concurrent.futures import ThreadPoolExecutor
 
-        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall", "-Wextra", "-fvisibility=hidden",
-              f"-I{INCLUDE}", f"-I{CSRC / 'host'}", f"-I{NLOHMANN}", f"-I{pybind11.get_include()}",
-              f"-I{sysconfig.get_paths()['include']}", "-o", out, *HOST_SOURCES,
-              f"-L{PKG}", "-lsmx", "-Wl,-rpath,$ORIGIN"])
+    objdir = PKG / "build" / "host"
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = ["-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wextra", "-fvisibility=hidden",
+             f"-I{INCLUDE}", f"-I{CSRC / 'host'}", f"-I{NLOHMANN}", f"-I{pybind11.get_include()}",
+             f"-I{sysconfig.get_paths()['include']}"]
+    headers = [d for d in HOST_DEPS if d.suffix == ".hpp"] + [INCLUDE / "smx.h"]
+
+    def compile_one(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        if force or _stale(obj, [src, *headers]):
+            _run(["g++", *flags, "-c", "-o", obj, src])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(compile_one, HOST_SOURCES))
+    _run(["g++", "-shared", "-o", out, *objs, f"-L{PKG}", "-lsmx", "-Wl,-rpath,$ORIGIN"])
     return out
 
 

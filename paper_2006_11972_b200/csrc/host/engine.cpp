@@ -1,2 +1,446 @@
-#include <pybind11/pybind11.h>
-void bind_engine(pybind11::module_&) {}
+// The engine: deterministic lockstep event loop over the smx executor (see engine.hpp).
+#include "stagemerge/engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <numeric>
+
+#include "smx.h"
+
+namespace stagemerge {
+
+namespace {
+
+void smx_ok(int rc, const char* what) {
+    if (rc == SMX_OK) return;
+    const std::string msg = std::string(what) + ": " + smx_last_error();
+    if (rc == SMX_ECONFIG) throw ConfigError(msg);
+    if (rc == SMX_EINTEGRITY) throw IntegrityError(msg);
+    throw std::runtime_error("device error: " + msg);
+}
+
+std::string hex16(std::uint64_t v) {
+    char b[20];
+    std::snprintf(b, sizeof b, "%016llx", static_cast<unsigned long long>(v));
+    return b;
+}
+
+constexpr const char* kTrialHp = "__trial";  // TRIAL mode: a per-trial constant hp defeats merging
+
+}  // namespace
+
+struct Engine::Gpu {
+    int device = 0;
+    smx_ctx* ctx = nullptr;
+    std::vector<int> free_entries;
+    std::map<CkptHandle, int> entry_of;  // checkpoints resident in this GPU's pool
+    std::vector<CkptHandle> handle_of;   // entry -> handle ("" = free)
+    std::vector<std::uint64_t> last_use; // LRU clock per entry
+};
+
+struct Engine::Worker {
+    int id = 0, gpu = 0, slot = 0;
+    bool busy = false;
+    Assignment a;
+    std::size_t cur = 0;
+    StepCount remaining = 0;
+};
+
+Engine::Engine(CompatKey key, EngineOptions opts) : key_(std::move(key)), opts_(std::move(opts)) {
+    if (opts_.devices.empty()) throw ConfigError("engine needs at least one device");
+    if (opts_.slots_per_gpu < 1 || opts_.ckpts_per_gpu < 1) throw ConfigError("bad slot / checkpoint counts");
+    if (opts_.trial_mode) {
+        key_.hp_set.push_back(kTrialHp);
+        std::sort(key_.hp_set.begin(), key_.hp_set.end());
+    }
+    plan_ = std::make_unique<SearchPlan>(key_);
+    smx_model_desc d{SMX_MODEL_MLP, opts_.max_batch, opts_.n_train, opts_.n_val, opts_.max_steps, opts_.gemm_mode,
+                     opts_.seed};
+    for (int dev : opts_.devices) {
+        auto g = std::make_unique<Gpu>();
+        g->device = dev;
+        smx_ok(smx_open(&d, dev, opts_.slots_per_gpu, opts_.ckpts_per_gpu, &g->ctx), "smx_open");
+        smx_set_graphs(g->ctx, opts_.use_graphs ? 1 : 0);
+        smx_param_count(g->ctx, nullptr, &p_alloc_);
+        g->handle_of.assign(static_cast<std::size_t>(opts_.ckpts_per_gpu), "");
+        g->last_use.assign(static_cast<std::size_t>(opts_.ckpts_per_gpu), 0);
+        for (int e = opts_.ckpts_per_gpu - 1; e >= 0; --e) g->free_entries.push_back(e);
+        gpus_.push_back(std::move(g));
+    }
+    // worker w -> GPU w % G, slot w / G: "lowest idle worker first" spreads paths over GPUs
+    const int G = static_cast<int>(gpus_.size());
+    for (int w = 0; w < G * opts_.slots_per_gpu; ++w) {
+        auto wk = std::make_unique<Worker>();
+        wk->id = w;
+        wk->gpu = w % G;
+        wk->slot = w / G;
+        workers_.push_back(std::move(wk));
+    }
+}
+
+Engine::~Engine() {
+    for (auto& g : gpus_)
+        if (g->ctx) smx_close(g->ctx);
+}
+
+std::vector<smx_ctx*> Engine::contexts() const {
+    std::vector<smx_ctx*> v;
+    for (const auto& g : gpus_) v.push_back(g->ctx);
+    return v;
+}
+
+void Engine::reset() {
+    for (auto& w : workers_)
+        if (w->busy) throw IntegrityError("reset while workers are busy");
+    plan_ = std::make_unique<SearchPlan>(key_);
+    for (auto& g : gpus_) {
+        g->entry_of.clear();
+        g->free_entries.clear();
+        std::fill(g->last_use.begin(), g->last_use.end(), 0);
+        for (int e = opts_.ckpts_per_gpu - 1; e >= 0; --e) {
+            g->handle_of[static_cast<std::size_t>(e)].clear();
+            g->free_entries.push_back(e);
+            smx_ckpt_free(g->ctx, e);
+        }
+        smx_reset_stats(g->ctx);
+    }
+    trial_index_.clear();
+    trial_cfg_.clear();
+    spilled_.clear();
+    root_owner_.clear();
+    stats_ = EngineStats{};
+    next_assignment_ = 0;
+}
+
+void Engine::upload_dataset(const float* x, const std::int32_t* y, const float* vx, const std::int32_t* vy) {
+    for (auto& g : gpus_) smx_ok(smx_dataset_upload(g->ctx, x, y, vx, vy), "smx_dataset_upload");
+    const std::int64_t rows = static_cast<std::int64_t>(opts_.n_train) + opts_.max_batch;
+    stats_.h2d_bytes += static_cast<std::int64_t>(gpus_.size()) *
+                        (rows * 784 * 4 + rows * 4 + static_cast<std::int64_t>(opts_.n_val) * (784 * 4 + 4));
+}
+
+std::uint64_t Engine::dataset_digest() {
+    std::uint64_t h = 0;
+    smx_ok(smx_dataset_digest(gpus_.front()->ctx, &h), "smx_dataset_digest");
+    return h;
+}
+
+InsertOutcome Engine::submit(const TrialRequest& in) {
+    TrialRequest req = in;
+    if (opts_.trial_mode) {
+        HpFunction tag;
+        tag.params["value"] = Rational(static_cast<std::int64_t>(in.study) * 1000003 + in.trial + 1);
+        req.config.sequences[kTrialHp] = make_sequence(kTrialHp, tag, req.config.total_steps);
+    }
+    if (req.config.total_steps > opts_.max_steps)
+        throw ConfigError("trial longer than the executor's max_steps (" + std::to_string(opts_.max_steps) + ")");
+    InsertOutcome out = plan_->insert_trial(req);
+    const TrialRef t{in.study, in.trial};
+    trial_index_[t] = {req.config.total_steps, out.node};
+    trial_cfg_[t] = in.config;
+    if (out.kind == InsertOutcome::Kind::kImmediate) stats_.trial_steps += req.config.total_steps;
+    return out;
+}
+
+bool Engine::cancel(const TrialRef& t) { return plan_->cancel_trial(t); }
+
+std::vector<TrialRef> Engine::trials() const {
+    std::vector<TrialRef> v;
+    for (const auto& kv : trial_index_) v.push_back(kv.first);
+    return v;
+}
+
+StepCount Engine::trial_end(const TrialRef& t) const { return trial_index_.at(t).first; }
+
+MetricHistory Engine::history(const TrialRef& t) const {
+    const auto& [end, leaf] = trial_index_.at(t);
+    MetricHistory h;
+    const auto path = plan_->path_to(leaf);
+    for (std::size_t i = 0; i < path.size(); ++i) {
+        const PlanNode& n = plan_->node(path[i]);
+        const StepCount hi = i + 1 < path.size() ? plan_->node(path[i + 1]).start_step : end;
+        for (const auto& [s, rec] : n.metrics)
+            if (s > n.start_step && s <= hi) h[s] = rec;
+    }
+    return h;
+}
+
+TimeUs Engine::est_us(NodeId n) const {
+    // deterministic cost model: proportional to the batch size at the node's start
+    const auto& cfg = plan_->node(n).config;
+    double bs = opts_.default_bs;
+    if (cfg.count(opts_.hp_bs)) bs = plan_->value_at(n, opts_.hp_bs, plan_->node(n).start_step);
+    return std::max<TimeUs>(1, static_cast<TimeUs>(bs));
+}
+
+std::set<NodeId> Engine::owned_roots() const {
+    std::set<NodeId> own;
+    const auto& roots = plan_->roots();
+    if (opts_.world <= 1) return {roots.begin(), roots.end()};
+    // LPT over root subtrees by step extent (deterministic; every rank computes the same map)
+    std::vector<NodeId> fresh;
+    for (NodeId r : roots)
+        if (!root_owner_.count(r)) fresh.push_back(r);
+    if (!fresh.empty()) {
+        std::map<NodeId, StepCount> work;
+        for (const PlanNode& n : plan_->nodes()) {
+            StepCount hi = n.start_step;
+            for (const auto& e : n.requests) hi = std::max(hi, e.end);
+            for (NodeId c : n.children) hi = std::max(hi, plan_->node(c).start_step);
+            NodeId r = n.id;
+            while (plan_->node(r).parent) r = *plan_->node(r).parent;
+            work[r] += hi - n.start_step;
+        }
+        std::vector<StepCount> load(static_cast<std::size_t>(opts_.world), 0);
+        for (const auto& [r, o] : root_owner_) load[static_cast<std::size_t>(o)] += work[r];
+        std::stable_sort(fresh.begin(), fresh.end(), [&](NodeId a, NodeId b) { return work[a] > work[b]; });
+        for (NodeId r : fresh) {
+            const auto o = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+            root_owner_[r] = o;
+            load[static_cast<std::size_t>(o)] += work[r];
+        }
+    }
+    for (const auto& [r, o] : root_owner_)
+        if (o == opts_.rank) own.insert(r);
+    return own;
+}
+
+std::set<NodeId> Engine::blocked_nodes() const {
+    std::set<NodeId> running;
+    for (const auto& w : workers_)
+        if (w->busy)
+            for (std::size_t i = w->cur; i < w->a.stages.size(); ++i) running.insert(w->a.stages[i].node);
+    if (opts_.world > 1) {
+        const std::set<NodeId> own = owned_roots();
+        for (const PlanNode& n : plan_->nodes()) {
+            NodeId r = n.id;
+            while (plan_->node(r).parent) r = *plan_->node(r).parent;
+            if (!own.count(r)) running.insert(n.id);
+        }
+    }
+    return running;
+}
+
+int Engine::alloc_entry(int gpu) {
+    Gpu& g = *gpus_[static_cast<std::size_t>(gpu)];
+    if (g.free_entries.empty()) {
+        // pool full: spill the least recently used entry to host memory (the checkpoint spill
+        // tier); a later LOAD brings it back with smx_ckpt_write
+        int victim = -1;
+        for (int e = 0; e < opts_.ckpts_per_gpu; ++e)
+            if (victim < 0 || g.last_use[static_cast<std::size_t>(e)] < g.last_use[static_cast<std::size_t>(victim)])
+                victim = e;
+        const CkptHandle h = g.handle_of[static_cast<std::size_t>(victim)];
+        if (!spilled_.count(h)) {
+            HostCkpt hc;
+            hc.w.resize(static_cast<std::size_t>(p_alloc_));
+            hc.m.resize(static_cast<std::size_t>(p_alloc_));
+            smx_ok(smx_ckpt_read(g.ctx, victim, hc.w.data(), hc.m.data(), &hc.step, &hc.offset), "smx_ckpt_read");
+            stats_.d2h_bytes += 8 * p_alloc_;
+            spilled_.emplace(h, std::move(hc));
+        }
+        g.entry_of.erase(h);
+        g.handle_of[static_cast<std::size_t>(victim)].clear();
+        smx_ckpt_free(g.ctx, victim);
+        g.free_entries.push_back(victim);
+        stats_.spills += 1;
+    }
+    const int e = g.free_entries.back();
+    g.free_entries.pop_back();
+    g.last_use[static_cast<std::size_t>(e)] = ++use_clock_;
+    return e;
+}
+
+// Pool entry holding checkpoint `h` on `gpu`, peer-copying it from another GPU if needed (K7).
+int Engine::ckpt_on(int gpu, const CkptHandle& h) {
+    Gpu& g = *gpus_[static_cast<std::size_t>(gpu)];
+    if (auto it = g.entry_of.find(h); it != g.entry_of.end()) {
+        g.last_use[static_cast<std::size_t>(it->second)] = ++use_clock_;
+        return it->second;
+    }
+    for (std::size_t o = 0; o < gpus_.size(); ++o) {
+        Gpu& src = *gpus_[o];
+        auto it = src.entry_of.find(h);
+        if (it == src.entry_of.end()) continue;
+        const int e = alloc_entry(gpu);
+        smx_ok(smx_ckpt_peer_copy(g.ctx, e, src.ctx, it->second), "smx_ckpt_peer_copy");
+        g.entry_of[h] = e;
+        g.handle_of[static_cast<std::size_t>(e)] = h;
+        stats_.peer_copies += 1;
+        return e;
+    }
+    if (auto it = spilled_.find(h); it != spilled_.end()) {
+        const int e = alloc_entry(gpu);
+        const HostCkpt& hc = it->second;
+        smx_ok(smx_ckpt_write(g.ctx, e, hc.w.data(), hc.m.data(), hc.step, hc.offset), "smx_ckpt_write");
+        stats_.h2d_bytes += 8 * p_alloc_;
+        g.entry_of[h] = e;
+        g.handle_of[static_cast<std::size_t>(e)] = h;
+        return e;
+    }
+    return -1;
+}
+
+void Engine::upload_hp(Worker& w, const Stage& s) {
+    const StepCount n = s.end - s.start;
+    if (n <= 0) return;
+    std::vector<float> rows(static_cast<std::size_t>(n) * SMX_HP_COLS);
+    const auto& cfg = plan_->node(s.node).config;
+    const std::string* names[SMX_HP_COLS] = {&opts_.hp_lr, &opts_.hp_momentum, &opts_.hp_wd, &opts_.hp_bs};
+    const double defaults[SMX_HP_COLS] = {opts_.default_lr, opts_.default_momentum, opts_.default_wd, opts_.default_bs};
+    for (int c = 0; c < SMX_HP_COLS; ++c) {
+        const bool tuned = cfg.count(*names[c]) > 0;
+        for (StepCount i = 0; i < n; ++i)
+            rows[static_cast<std::size_t>(i) * SMX_HP_COLS + c] =
+                static_cast<float>(tuned ? plan_->value_at(s.node, *names[c], s.start + i) : defaults[c]);
+    }
+    smx_ok(smx_hp_upload(gpus_[static_cast<std::size_t>(w.gpu)]->ctx, w.slot, s.start, n, rows.data()), "smx_hp_upload");
+    stats_.h2d_bytes += static_cast<std::int64_t>(rows.size() * sizeof(float));
+}
+
+void Engine::begin_stage(Worker& w) {
+    const Stage& s = w.a.stages[w.cur];
+    upload_hp(w, s);
+    w.remaining = s.end - s.start;
+}
+
+void Engine::start(const Assignment& a) {
+    Worker& w = *workers_[static_cast<std::size_t>(a.worker)];
+    w.busy = true;
+    w.a = a;
+    w.cur = 0;
+    smx_ctx* ctx = gpus_[static_cast<std::size_t>(w.gpu)]->ctx;
+    const Stage& first = a.stages.front();
+    if (first.resume) {
+        const PlanNode& n = plan_->node(first.resume->node);
+        const auto it = n.ckpts.find(first.resume->step);
+        if (it == n.ckpts.end())
+            throw IntegrityError("resume checkpoint missing at node " + std::to_string(first.resume->node));
+        const int e = ckpt_on(w.gpu, it->second);
+        if (e < 0) throw IntegrityError("checkpoint " + it->second + " is not resident on any GPU");
+        smx_ok(smx_slot_load(ctx, w.slot, e), "smx_slot_load");
+        stats_.loads += 1;
+    } else {
+        if (first.start != 0) throw IntegrityError("scratch stage must start at step 0");
+        smx_ok(smx_slot_init(ctx, w.slot), "smx_slot_init");
+        stats_.inits += 1;
+    }
+    stats_.assignments += 1;
+    begin_stage(w);
+}
+
+void Engine::dispatch() {
+    std::vector<int> idle;
+    for (const auto& w : workers_)
+        if (!w->busy) idle.push_back(w->id);
+    if (idle.empty() || !plan_->has_pending()) return;
+    TreeBuildContext ctx;
+    ctx.running = blocked_nodes();
+    ctx.eval_intervals = opts_.eval_intervals;
+    const auto as = schedule(*plan_, ctx, idle, [this](NodeId n) { return est_us(n); }, next_assignment_);
+    next_assignment_ += static_cast<int>(as.size());
+    for (const Assignment& a : as) start(a);
+}
+
+void Engine::finish_stages(std::vector<Worker*>& done) {
+    // SAVE (every stage end) in worker order
+    for (Worker* w : done) {
+        const Stage& s = w->a.stages[w->cur];
+        if (s.end <= s.start) continue;
+        const CkptHandle h = hex16(plan_->prefix_digest_at(s.node, s.end));
+        const PlanNode& n = plan_->node(s.node);
+        Gpu& g = *gpus_[static_cast<std::size_t>(w->gpu)];
+        if (!n.ckpts.count(s.end) || !g.entry_of.count(h)) {
+            bool resident = false;
+            for (const auto& og : gpus_) resident = resident || og->entry_of.count(h);
+            resident = resident || spilled_.count(h);
+            if (!resident) {
+                const int e = alloc_entry(w->gpu);
+                smx_ok(smx_slot_save(g.ctx, w->slot, e), "smx_slot_save");
+                g.entry_of[h] = e;
+                g.handle_of[static_cast<std::size_t>(e)] = h;
+                stats_.saves += 1;
+            }
+        }
+        plan_->record_checkpoint(s.node, s.end, h);
+    }
+    // EVAL, batched per GPU
+    std::map<int, std::vector<Worker*>> by_gpu;
+    for (Worker* w : done)
+        if (w->a.stages[w->cur].eval_at_end) by_gpu[w->gpu].push_back(w);
+    std::map<int, MetricRecord> records;
+    for (auto& [gi, ws] : by_gpu) {
+        std::vector<int> slots;
+        for (Worker* w : ws) slots.push_back(w->slot);
+        std::vector<double> out(slots.size() * SMX_MET_COLS);
+        smx_ok(smx_eval(gpus_[static_cast<std::size_t>(gi)]->ctx, static_cast<int>(slots.size()), slots.data(), out.data()),
+               "smx_eval");
+        stats_.evals += static_cast<std::int64_t>(slots.size());
+        stats_.d2h_bytes += static_cast<std::int64_t>(out.size() * sizeof(double));
+        for (std::size_t i = 0; i < ws.size(); ++i)
+            records[ws[i]->id] = MetricRecord{{"val_acc", out[i * SMX_MET_COLS + SMX_MET_VAL_ACC]},
+                                              {"val_loss", out[i * SMX_MET_COLS + SMX_MET_VAL_LOSS]}};
+    }
+    // aggregate: record metrics, fan out completions, advance workers (ascending id)
+    for (Worker* w : done) {
+        const Stage s = w->a.stages[w->cur];
+        if (auto it = records.find(w->id); it != records.end()) {
+            for (const CompletedRequest& c : plan_->record_metrics(s.node, s.end, it->second)) {
+                stats_.trial_steps += static_cast<std::int64_t>(c.subscribers.size()) * c.end;
+                if (on_complete_) on_complete_(*this, c);
+            }
+        }
+        w->cur += 1;
+        if (w->cur < w->a.stages.size())
+            begin_stage(*w);
+        else
+            w->busy = false;
+    }
+}
+
+void Engine::run() {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int G = static_cast<int>(gpus_.size());
+    for (;;) {
+        dispatch();
+        // stages with nothing (left) to train finish immediately: eval-only stages
+        for (;;) {
+            std::vector<Worker*> done;
+            for (auto& w : workers_)
+                if (w->busy && w->remaining == 0) done.push_back(w.get());
+            if (done.empty()) break;
+            finish_stages(done);
+            dispatch();
+        }
+        std::vector<Worker*> active;
+        for (auto& w : workers_)
+            if (w->busy) active.push_back(w.get());
+        if (active.empty()) break;
+        StepCount k = active.front()->remaining;
+        for (Worker* w : active) k = std::min(k, w->remaining);
+        for (int gi = 0; gi < G; ++gi) {
+            std::vector<int> slots;
+            for (Worker* w : active)
+                if (w->gpu == gi) slots.push_back(w->slot);
+            if (slots.empty()) continue;
+            smx_ok(smx_train(gpus_[static_cast<std::size_t>(gi)]->ctx, static_cast<int>(slots.size()), slots.data(),
+                             static_cast<int>(k)),
+                   "smx_train");
+            stats_.locksteps += k;
+        }
+        for (Worker* w : active) w->remaining -= k;
+        stats_.stage_steps += k * static_cast<StepCount>(active.size());
+    }
+    for (auto& g : gpus_) smx_ok(smx_sync(g->ctx), "smx_sync");
+    std::int64_t launches = 0;
+    for (auto& g : gpus_) {
+        smx_stats st{};
+        smx_get_stats(g->ctx, &st);
+        launches += st.launches;
+    }
+    stats_.kernel_launches = launches;
+    stats_.wall_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace stagemerge

@@ -430,6 +430,28 @@ int smx_dataset_digest(smx_ctx* c, uint64_t* out) {
     });
 }
 
+int smx_dataset_upload(smx_ctx* c, const float* x, const int32_t* y, const float* vx, const int32_t* vy) {
+    return guard([&] {
+        if (!x || !y || !vx || !vy) fail(SMX_ECONFIG, "null dataset buffer");
+        cudaSetDevice(c->device);
+        const long long rows = (long long)c->d.n_train + c->d.max_batch;
+        ck(cudaMemcpyAsync(c->xtrain, x, sizeof(float) * rows * kD0, cudaMemcpyHostToDevice, c->stream), "x H2D");
+        ck(cudaMemcpyAsync(c->ytrain, y, sizeof(int) * rows, cudaMemcpyHostToDevice, c->stream), "y H2D");
+        ck(cudaMemcpyAsync(c->xval, vx, sizeof(float) * (long long)c->d.n_val * kD0, cudaMemcpyHostToDevice, c->stream),
+           "vx H2D");
+        ck(cudaMemcpyAsync(c->yval, vy, sizeof(int) * c->d.n_val, cudaMemcpyHostToDevice, c->stream), "vy H2D");
+        ck(cudaStreamSynchronize(c->stream), "dataset sync");
+    });
+}
+
+int smx_host_alloc(uint64_t bytes, void** out) {
+    return guard([&] { ck(cudaMallocHost(out, bytes), "cudaMallocHost"); });
+}
+
+int smx_host_free(void* p) {
+    return guard([&] { ck(cudaFreeHost(p), "cudaFreeHost"); });
+}
+
 int smx_hp_upload(smx_ctx* c, int slot, int64_t step0, int64_t n, const float* hp) {
     return guard([&] {
         check_slot(c, slot);

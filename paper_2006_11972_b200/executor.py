@@ -23,7 +23,8 @@ MET_COLS = 2
 
 # Every symbol include/smx.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "smx_open", "smx_close", "smx_param_count", "smx_dataset_digest", "smx_hp_upload", "smx_slot_init",
+    "smx_open", "smx_close", "smx_param_count", "smx_dataset_digest", "smx_dataset_upload", "smx_host_alloc",
+    "smx_host_free", "smx_hp_upload", "smx_slot_init",
     "smx_slot_load", "smx_slot_save", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
     "smx_slot_write", "smx_ckpt_read", "smx_ckpt_write", "smx_train", "smx_eval", "smx_losses", "smx_sync",
     "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel",
@@ -80,6 +81,9 @@ def load_library() -> ctypes.CDLL:
             "smx_param_count": [P, ctypes.POINTER(I64), ctypes.POINTER(I64)],
             "smx_dataset_digest": [P, ctypes.POINTER(ctypes.c_uint64)],
             "smx_hp_upload": [P, I, I64, I64, FP],
+            "smx_dataset_upload": [P, FP, P, FP, P],
+            "smx_host_alloc": [ctypes.c_uint64, ctypes.POINTER(P)],
+            "smx_host_free": [P],
             "smx_slot_init": [P, I],
             "smx_slot_load": [P, I, I],
             "smx_slot_save": [P, I, I],
@@ -166,6 +170,12 @@ class Executor:
         out = ctypes.c_uint64()
         _check(self._lib.smx_dataset_digest(self._ctx, ctypes.byref(out)))
         return out.value
+
+    def dataset_upload(self, x: np.ndarray, y: np.ndarray, vx: np.ndarray, vy: np.ndarray) -> None:
+        arrs = [np.ascontiguousarray(a) for a in (x, y, vx, vy)]
+        assert arrs[0].dtype == np.float32 and arrs[1].dtype == np.int32
+        _check(self._lib.smx_dataset_upload(self._ctx, _fp(arrs[0]), arrs[1].ctypes.data, _fp(arrs[2]),
+                                            arrs[3].ctypes.data))
 
     def hp_upload(self, slot: int, step0: int, rows: np.ndarray) -> None:
         rows = np.ascontiguousarray(rows, dtype=np.float32).reshape(-1, HP_COLS)
