@@ -116,7 +116,11 @@ void bind_engine(py::module_& m) {
                                     rec.count("val_acc") ? rec.at("val_acc") : 0.0);
                  return v;
              })
-        .def("owned_roots", [](Engine& e) { return std::vector<NodeId>(e.owned_roots().begin(), e.owned_roots().end()); })
+        .def("owned_roots",
+             [](Engine& e) {
+                 const std::set<NodeId> own = e.owned_roots();
+                 return std::vector<NodeId>(own.begin(), own.end());
+             })
         .def("dataset_digest", [](Engine& e) { return e.dataset_digest(); })
         .def("context_ptrs",
              [](Engine& e) {

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #include "smx.h"
@@ -400,6 +401,7 @@ void Engine::finish_stages(std::vector<Worker*>& done) {
 }
 
 void Engine::run() {
+    static const bool trace = std::getenv("SMX_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     const int G = static_cast<int>(gpus_.size());
     for (;;) {
@@ -419,6 +421,8 @@ void Engine::run() {
         if (active.empty()) break;
         StepCount k = active.front()->remaining;
         for (Worker* w : active) k = std::min(k, w->remaining);
+        if (trace) std::fprintf(stderr, "[engine] active=%zu k=%lld stage_steps=%lld\n", active.size(),
+                                static_cast<long long>(k), static_cast<long long>(stats_.stage_steps));
         for (int gi = 0; gi < G; ++gi) {
             std::vector<int> slots;
             for (Worker* w : active)
