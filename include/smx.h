@@ -148,6 +148,12 @@ int smx_reset_stats(smx_ctx* ctx);
  * `n` slots, 1 = K6 fork copy of `n` checkpoints.  Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
 
+/* Test hook: one ungrouped GEMM C[M x N] = A op B on the device through the executor's GEMM
+ * kernels (gemm_mode of the context): am/bm = 0 when A(m,k) = A[m*lda+k] / B(n,k) = B[n*ldb+k],
+ * 1 when A(m,k) = A[k*lda+m] / B(n,k) = B[k*ldb+n].  Host buffers in and out; synchronous. */
+int smx_test_gemm(smx_ctx* ctx, int am, int bm, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                  float* C);
+
 const char* smx_last_error(void);
 const char* smx_version(void);
 

@@ -130,6 +130,29 @@ __global__ void colsum_kernel(StepCtx c, const float* act, long long act_stride,
     grad[grad_stride * slot + db_off + n] = s;
 }
 
+// Tensor-core mode: the same sums with 8 row-lanes per column and a fixed-order combine
+// (deterministic and grouping-invariant; not the oracle's sequential order, which only the exact
+// mode promises).  grid: (ceil(N/32), groups), block 256.
+__global__ void colsum_fast_kernel(StepCtx c, const float* act, long long act_stride, long long dy_off, int ld, int N,
+                                   float* grad, long long grad_stride, long long db_off) {
+    const int slot = c.slots[blockIdx.y];
+    const int B = (int)hp_row(c, slot)[3];
+    const int col = threadIdx.x & 31, lane_r = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + col;
+    __shared__ float part[8][33];
+    const float* dY = act + act_stride * slot + dy_off;
+    float s = 0.0f;
+    if (n < N)
+        for (int r = lane_r; r < B; r += 8) s = __fadd_rn(s, dY[(long long)r * ld + n]);
+    part[lane_r][col] = s;
+    __syncthreads();
+    if (lane_r == 0 && n < N) {
+        float t = part[0][col];
+        for (int i = 1; i < 8; ++i) t = __fadd_rn(t, part[i][col]);
+        grad[grad_stride * slot + db_off + n] = t;
+    }
+}
+
 // ---- K5: fused SGD / momentum / weight-decay update ----------------------------------
 //   g' = fma(wd, w, g);  m = fma(mu, m, g');  w = fma(-lr, m, w)
 // (PyTorch SGD semantics, no dampening / Nesterov).  (lr, mu, wd) come from the

@@ -20,6 +20,7 @@
 #include "../../include/smx.h"
 #include "kernels/common.cuh"
 #include "kernels/gemm_simt.cuh"
+#include "kernels/gemm_tc.cuh"
 #include "kernels/step_kernels.cuh"
 
 using namespace smx;
@@ -105,10 +106,44 @@ GemmArgs base_args(smx_ctx* c, const int* d_slots) {
 }
 
 template <int AM, int BMODE, int EPI>
+void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
+    static bool configured = false;  // per instantiation (device-independent attribute)
+    if (!configured) {
+        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc::kSmem),
+           "tc smem attribute");
+        configured = true;
+    }
+    if ((a.a.ld & 3) || (a.b.ld & 3))
+        fail(SMX_ECONFIG, "tensor-core GEMM needs 16-byte aligned operand rows (ld % 4 == 0)");
+    const int mt = (m_max + tc::kBM - 1) / tc::kBM;
+    dim3 grid((a.N + tc::kBN - 1) / tc::kBN, mt, groups);
+    tc::gemm_tc_kernel<AM, BMODE, EPI><<<grid, tc::kThreads, tc::kSmem, c->stream>>>(a, tc::kBN);
+    launch_check(c, "gemm_tc");
+}
+
+template <int AM, int BMODE, int EPI>
 void gemm(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
+    if (c->d.gemm_mode == SMX_GEMM_TC) {
+        constexpr int tepi = EPI == kEpiStore ? tc::kTcStore : EPI == kEpiBiasRelu ? tc::kTcBiasRelu
+                             : EPI == kEpiBias ? tc::kTcBias : tc::kTcMask;
+        tc_launch<AM, BMODE, tepi>(c, a, groups, m_max);
+        return;
+    }
     dim3 grid((a.N + kTN - 1) / kTN, (m_max + kTM - 1) / kTM, groups);
     gemm_simt_kernel<AM, BMODE, EPI><<<grid, 256, 0, c->stream>>>(a);
     launch_check(c, "gemm_simt");
+}
+
+// Bias gradient of one layer: db[n] = sum over the batch of dY[r][n].
+void colsum(smx_ctx* c, const StepCtx& sc, int groups, long long dy_off, int ld, int N, long long db_off) {
+    if (c->d.gemm_mode == SMX_GEMM_TC)
+        colsum_fast_kernel<<<dim3((N + 31) / 32, groups), 256, 0, c->stream>>>(sc, c->act, kActStride, dy_off, ld, N,
+                                                                                c->grad, kPAlloc, db_off);
+    else
+        colsum_kernel<<<dim3((N + 127) / 128, groups), 128, 0, c->stream>>>(sc, c->act, kActStride, dy_off, ld, N,
+                                                                             c->grad, kPAlloc, db_off);
+    launch_check(c, "colsum");
 }
 
 // One lockstep of the MLP over `n` slots listed in device array d_slots.
@@ -153,7 +188,14 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
         loss_train_kernel<<<n, kMaxBatch, 0, c->stream>>>(sc, c->ytrain, c->d.n_train - 1, A, AS, c->loss);
         launch_check(c, "loss_train");
         // ---- layer 3 grads
-        {
+        if (c->d.gemm_mode == SMX_GEMM_TC) {
+            GemmArgs g = base_args(c, d_slots);  // gW3^T[k][c] = sum_r H2[r][k] dZ[r][c], stored transposed
+            g.a = Opnd{A + kActH2, AS, kH, 0};
+            g.b = Opnd{A + kActDZ, AS, kCP, 0};
+            g.c = G + kOffW3; g.c_stride = kPAlloc; g.ldc = kH;
+            g.M = kH; g.N = kCP; g.K = mb; g.k_is_bs = 1;
+            tc_launch<1, 1, tc::kTcStoreT>(c, g, n, kH);
+        } else {
             GemmArgs g = base_args(c, d_slots);  // gW3[c][k] = sum_r dZ[r][c] H2[r][k]
             g.a = Opnd{A + kActDZ, AS, kCP, 0};
             g.b = Opnd{A + kActH2, AS, kH, 0};
@@ -161,8 +203,7 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             g.M = kCP; g.N = kH; g.K = mb; g.k_is_bs = 1;
             gemm<1, 1, kEpiStore>(c, g, n, kCP);
         }
-        colsum_kernel<<<dim3(1, n), 128, 0, c->stream>>>(sc, A, AS, kActDZ, kCP, kCP, G, kPAlloc, kOffB3);
-        launch_check(c, "colsum3");
+        colsum(c, sc, n, kActDZ, kCP, kCP, kOffB3);
         {
             GemmArgs g = base_args(c, d_slots);  // dH2[r][k] = (H2>0) sum_c dZ[r][c] W3[c][k]
             g.a = Opnd{A + kActDZ, AS, kCP, 0};
@@ -181,8 +222,7 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             g.M = kH; g.N = kH; g.K = mb; g.k_is_bs = 1;
             gemm<1, 1, kEpiStore>(c, g, n, kH);
         }
-        colsum_kernel<<<dim3(2, n), 128, 0, c->stream>>>(sc, A, AS, kActDH2, kH, kH, G, kPAlloc, kOffB2);
-        launch_check(c, "colsum2");
+        colsum(c, sc, n, kActDH2, kH, kH, kOffB2);
         {
             GemmArgs g = base_args(c, d_slots);
             g.a = Opnd{A + kActDH2, AS, kH, 0};
@@ -201,8 +241,7 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             g.M = kH; g.N = kD0; g.K = mb; g.k_is_bs = 1;
             gemm<1, 1, kEpiStore>(c, g, n, kH);
         }
-        colsum_kernel<<<dim3(2, n), 128, 0, c->stream>>>(sc, A, AS, kActDH1, kH, kH, G, kPAlloc, kOffB1);
-        launch_check(c, "colsum1");
+        colsum(c, sc, n, kActDH1, kH, kH, kOffB1);
     }
     // ---- K5 update + advance
     if (c->timing) cudaEventRecord(c->ev[2], c->stream);
@@ -328,7 +367,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         if (d.n_train < 256 || (d.n_train & (d.n_train - 1))) fail(SMX_ECONFIG, "n_train must be a power of two >= 256");
         if (d.n_val < 128 || d.n_val % 128) fail(SMX_ECONFIG, "n_val must be a positive multiple of 128");
         if (d.max_steps < 1) fail(SMX_ECONFIG, "max_steps must be >= 1");
-        if (d.gemm_mode != SMX_GEMM_EXACT) fail(SMX_ECONFIG, "gemm_mode not available in this build");
+        if (d.gemm_mode != SMX_GEMM_EXACT && d.gemm_mode != SMX_GEMM_TC) fail(SMX_ECONFIG, "bad gemm_mode");
         if (n_slots < 1 || n_ckpts < 0) fail(SMX_ECONFIG, "bad slot/checkpoint counts");
         int ndev = 0;
         ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -800,6 +839,53 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
         *ms_per_launch = ms / reps;
+    });
+}
+
+int smx_test_gemm(smx_ctx* c, int am, int bm, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                  float* C) {
+    return guard([&] {
+        if (M < 1 || N < 1 || K < 1) fail(SMX_ECONFIG, "bad GEMM shape");
+        cudaSetDevice(c->device);
+        const size_t na = (size_t)(am ? K : M) * lda, nb = (size_t)(bm ? K : N) * ldb, nc = (size_t)M * N;
+        float *dA, *dB, *dC;
+        int* dslot;
+        SlotState* dst;
+        ck(cudaMalloc(&dA, na * 4), "A");
+        ck(cudaMalloc(&dB, nb * 4), "B");
+        ck(cudaMalloc(&dC, nc * 4), "C");
+        ck(cudaMalloc(&dslot, 4), "slot");
+        ck(cudaMalloc(&dst, sizeof(SlotState)), "st");
+        ck(cudaMemcpy(dA, A, na * 4, cudaMemcpyHostToDevice), "A H2D");
+        ck(cudaMemcpy(dB, B, nb * 4, cudaMemcpyHostToDevice), "B H2D");
+        ck(cudaMemset(dslot, 0, 4), "slot zero");
+        ck(cudaMemset(dst, 0, sizeof(SlotState)), "st zero");
+        ck(cudaMemset(dC, 0xFF, nc * 4), "C poison");
+        GemmArgs g{};
+        g.slots = dslot;
+        g.st = dst;
+        g.hp = c->hp;
+        g.hp_cap = c->d.max_steps;
+        g.n_train_mask = c->d.n_train - 1;
+        g.a = Opnd{dA, 0, lda, 0};
+        g.b = Opnd{dB, 0, ldb, 0};
+        g.c = dC;
+        g.ldc = N;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        const int sel = am * 2 + bm;
+        if (sel == 0) gemm<0, 0, kEpiStore>(c, g, 1, M);
+        if (sel == 1) gemm<0, 1, kEpiStore>(c, g, 1, M);
+        if (sel == 2) gemm<1, 0, kEpiStore>(c, g, 1, M);
+        if (sel == 3) gemm<1, 1, kEpiStore>(c, g, 1, M);
+        ck(cudaStreamSynchronize(c->stream), "gemm sync");
+        ck(cudaMemcpy(C, dC, nc * 4, cudaMemcpyDeviceToHost), "C D2H");
+        cudaFree(dA);
+        cudaFree(dB);
+        cudaFree(dC);
+        cudaFree(dslot);
+        cudaFree(dst);
     });
 }
 

@@ -27,7 +27,7 @@ EXPORTS = (
     "smx_host_free", "smx_hp_upload", "smx_slot_init",
     "smx_slot_load", "smx_slot_save", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
     "smx_slot_write", "smx_ckpt_read", "smx_ckpt_write", "smx_train", "smx_eval", "smx_losses", "smx_sync",
-    "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel",
+    "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel", "smx_test_gemm",
     "smx_last_error", "smx_version",
 )
 
@@ -103,6 +103,7 @@ def load_library() -> ctypes.CDLL:
             "smx_get_stats": [P, ctypes.POINTER(Stats)],
             "smx_reset_stats": [P],
             "smx_bench_kernel": [P, I, I, I, ctypes.POINTER(ctypes.c_double)],
+            "smx_test_gemm": [P, I, I, I, I, I, FP, I, FP, I, FP],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)
@@ -258,6 +259,20 @@ class Executor:
 
     def reset_stats(self) -> None:
         _check(self._lib.smx_reset_stats(self._ctx))
+
+    def test_gemm(self, A: np.ndarray, B: np.ndarray, a_mn: bool, b_mn: bool, M: int | None = None,
+                  N: int | None = None) -> np.ndarray:
+        """C = A_logical @ B_logical^T where A_logical is A (a_mn False, [M,K]) or A.T (a_mn True,
+        A stored [K,>=M], leading dimension = A.shape[1]); likewise B ([N,K] or stored [K,>=N])."""
+        A = np.ascontiguousarray(A, np.float32)
+        B = np.ascontiguousarray(B, np.float32)
+        K = A.shape[0] if a_mn else A.shape[1]
+        M = M if M is not None else (A.shape[1] if a_mn else A.shape[0])
+        N = N if N is not None else (B.shape[1] if b_mn else B.shape[0])
+        C = np.empty((M, N), np.float32)
+        _check(self._lib.smx_test_gemm(self._ctx, int(a_mn), int(b_mn), M, N, K, _fp(A), A.shape[1], _fp(B),
+                                       B.shape[1], _fp(C)))
+        return C
 
     def bench_kernel(self, kind: int, n: int, reps: int) -> float:
         out = ctypes.c_double()
