@@ -230,7 +230,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--gemm", default=os.environ.get("SMX_BENCH_GEMM", "exact"), choices=["exact", "tc"])
+    ap.add_argument("--gemm", default=os.environ.get("SMX_BENCH_GEMM", "tc"), choices=["exact", "tc"])
     ap.add_argument("--slots", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -297,31 +297,44 @@ def main():
     for p in pinned:
         lib.smx_host_free(p)
 
-    # ---- per-kernel roofline: K5 update and K6 fork timed standalone on the engine's context
+    # ---- per-kernel roofline: standalone CUDA-event timing of the dominant kernels on a fresh
+    # 64-slot context of the same GPU (bs 128, the study's typical active set)
     pk = peaks()
-    ctx = ctypes.c_void_p(eng.context_ptrs()[0])
-    ms_u = ctypes.c_double()
-    n_upd = min(args.slots, 64)
-    assert lib.smx_bench_kernel(ctx, 0, n_upd, 50, ctypes.byref(ms_u)) == 0
-    ms_f = ctypes.c_double()
-    assert lib.smx_bench_kernel(ctx, 1, 16, 50, ctypes.byref(ms_f)) == 0
-    P, PALLOC = 269322, 270912
-    upd_bytes = 20 * P * n_upd
-    fork_bytes = 16 * P * 16
-    upd_gbs = upd_bytes / (ms_u.value * 1e-3) / 1e9
-    fork_gbs = fork_bytes / (ms_f.value * 1e-3) / 1e9
+    n_k = 64
+    kx = ex.Executor(n_slots=n_k, n_ckpts=16, device=local, max_steps=64, gemm_mode=gemm_mode)
+    for s_ in range(n_k):
+        kx.slot_init(s_)
+        kx.hp_upload(s_, 0, np.tile(np.float32([0.05, 0.9, 1e-4, 128]), (64, 1)))
+    kx.train(list(range(n_k)), 1)  # produce activations / gradients once
+    kx.sync()
+    ms = {kind: kx.bench_kernel(kind, n_k if kind != 1 else 16, 30) for kind in (0, 1, 2, 3)}
+    kx.close()
+    P = 269322
+    upd_bytes, fork_bytes = 20 * P * n_k, 16 * P * 16
+    gemm_flops = 2 * 128 * 256 * 784 * n_k  # per launch, both layer-1 GEMMs at bs 128
+    tc_peak = pk["bf16_tflops"]
+
+    def hbm(name, b, t, **kw):
+        a = b / (t * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": a, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": a / pk["hbm_gbs"],
+                "bytes_per_launch": b, "ms_per_launch": t, "peak_src": pk["src"], **kw}
+
+    def tensor(name, f, t):
+        a = f / (t * 1e-3) / 1e12
+        return {"bound": "tensor", "achieved": a, "peak": tc_peak, "unit": "TFLOP/s", "frac": a / tc_peak,
+                "flops_per_launch": f, "ms_per_launch": t, "peak_src": pk["src"] + " bf16 dense",
+                "note": "fp32-equivalent flops; 3xTF32 issues 3 kind::tf32 MMAs (tf32 = bf16/2) per product, so "
+                        "the mode's own ceiling is bf16/6 = %.0f TFLOP/s" % (tc_peak / 6)}
+
     kernels = {
-        "K5_update": {"bound": "hbm", "achieved": upd_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                      "frac": upd_gbs / pk["hbm_gbs"], "bytes_per_launch": upd_bytes, "slots": n_upd,
-                      "ms_per_launch": ms_u.value},
-        "K6_fork": {"bound": "hbm", "achieved": fork_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": fork_gbs / pk["hbm_gbs"], "bytes_per_launch": fork_bytes, "checkpoints": 16,
-                    "ms_per_launch": ms_f.value},
+        "K1_fwd1_gemm": tensor("fwd1", gemm_flops, ms[2]),
+        "K3_wgrad1_gemm": tensor("wgrad1", gemm_flops, ms[3]),
+        "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_k),
+        "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=16),
     }
-    # GEMM share: timing-mode locksteps of the study's own slot mix
-    roofline = dict(kernels["K5_update"])
+    roofline = dict(kernels["K1_fwd1_gemm"])
     roofline["traffic"] = None
-    roofline["kernel"] = "K5 fused SGD/momentum/wd update (sgd_update_kernel)"
+    roofline["kernel"] = "gemm_tc_kernel<0,0,BiasRelu> (layer-1 forward, 64 groups x 128x256x784)"
 
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -145,7 +145,9 @@ int smx_set_graphs(smx_ctx* ctx, int enabled); /* capture lockstep sequences in 
 int smx_get_stats(smx_ctx* ctx, smx_stats* out);
 int smx_reset_stats(smx_ctx* ctx);
 /* Standalone launches of one kernel class for roofline measurement: kind 0 = K5 update over
- * `n` slots, 1 = K6 fork copy of `n` checkpoints.  Returns mean CUDA-event ms per launch. */
+ * `n` slots, 1 = K6 fork copy of `n` checkpoints, 2 = the layer-1 forward GEMM over `n` slots,
+ * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size).
+ * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
 
 /* Test hook: one ungrouped GEMM C[M x N] = A op B on the device through the executor's GEMM

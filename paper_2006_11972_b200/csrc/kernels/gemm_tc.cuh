@@ -29,17 +29,18 @@ namespace tc {
 constexpr int kBM = 128;
 constexpr int kBN = 128;                         // N tile (the last tile may be narrower)
 constexpr int kKC = 32;                          // K elements per pipeline chunk
+constexpr int kKQ = kKC / 4;                     // 16-byte k-quads per chunk
 constexpr int kThreads = 256;
-// raw (as copied) tiles: K-contiguous rows of 32 k padded to 36 floats, or 32 k-rows of 128
+// raw (as copied) tiles: K-contiguous rows of kKC k padded by 4 floats, or kKC k-rows of 128
 constexpr int kRawLdK = kKC + 4;                 // floats per row, K-contiguous raw tile
 constexpr int kRawLdMN = kBM + 4;                // floats per k-row, row-contiguous raw tile
 constexpr int kRawTile = kBM * kRawLdK * 4;      // 18432 B >= kKC * kRawLdMN * 4 = 16896
 constexpr int kRawStage = 2 * kRawTile;          // A, B
 // K-major canonical: (row r, k) at (k/4)*kLbo + (r/8)*128 + (r%8)*16 + (k%4)*4  (SBO = 128)
 constexpr int kLbo = kBM * 16 + 16;              // 2064: padding keeps the split pass conflict-free
-constexpr int kTile = (kKC / 4) * kLbo;          // 16512 per operand per hi/lo
+constexpr int kTile = kKQ * kLbo;                // 16512 per operand per hi/lo
 constexpr int kHiLo = 4 * kTile;                 // A_hi A_lo B_hi B_lo
-constexpr int kSmem = 2 * kRawStage + 2 * kHiLo + 64;
+constexpr int kSmem = 2 * kRawStage + 2 * kHiLo + 64;  // ~201 KB: one CTA per SM
 constexpr int kTmemCols = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -99,9 +100,9 @@ template <int MN>
 __device__ __forceinline__ void load_raw(const float* g, int ld, int r0, int rows, int rlim, int k0, int klim,
                                          uint32_t dst) {
     if (MN == 0) {
-        const int units = rows * (kKC / 4);  // (row, k-quad): a warp reads 4 rows x 128 B
+        const int units = rows * kKQ;  // (row, k-quad): a warp reads 4 rows x 128 B
         for (int u = threadIdx.x; u < units; u += kThreads) {
-            const int r = u >> 3, kq = u & 7;
+            const int r = u / kKQ, kq = u % kKQ;
             const int row = r0 + r, k = k0 + kq * 4;
             const int valid = row < rlim ? max(0, min(4, klim - k)) : 0;
             cp16(dst + (r * kRawLdK + kq * 4) * 4, valid ? g + (long long)row * ld + k : g, valid * 4);
@@ -132,7 +133,7 @@ __device__ __forceinline__ void split_store(float4 v, char* hi, char* lo, uint32
 template <int MN>
 __device__ __forceinline__ void split_tile(const char* raw, int rows, char* hi, char* lo) {
     if (MN == 0) {
-        const int units = rows * (kKC / 4);  // consecutive threads: consecutive rows, same k-quad
+        const int units = rows * kKQ;  // consecutive threads: consecutive rows, same k-quad
         for (int u = threadIdx.x; u < units; u += kThreads) {
             const int r = u % rows, kq = u / rows;
             const float4 v = *reinterpret_cast<const float4*>(raw + (r * kRawLdK + kq * 4) * 4);
@@ -140,7 +141,7 @@ __device__ __forceinline__ void split_tile(const char* raw, int rows, char* hi, 
         }
     } else {
         const int quads = rows >> 2;
-        const int units = quads * (kKC / 4);  // 4 rows x 4 k per thread, transposed in registers
+        const int units = quads * kKQ;  // 4 rows x 4 k per thread, transposed in registers
         for (int u = threadIdx.x; u < units; u += kThreads) {
             const int rq = u % quads, kq = u / quads;
             float4 c[4];

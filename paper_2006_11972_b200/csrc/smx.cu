@@ -831,6 +831,37 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             cudaEventRecord(c->ev[6], c->stream);
             for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
             cudaEventRecord(c->ev[7], c->stream);
+        } else if (kind == 2 || kind == 3) {
+            // the two largest GEMMs of a lockstep at bs = 128 over n slots: 2 = fwd1 (X W1^T),
+            // 3 = wgrad1 (dH1^T X); the slots' hp rows must hold bs = 128 at their current step
+            if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
+            std::vector<int> v(n);
+            for (int i = 0; i < n; ++i) v[i] = i;
+            ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+            GemmArgs g = base_args(c, c->scratch_slots);
+            const long long SW = c->slab_stride();
+            if (kind == 2) {
+                g.a = Opnd{c->xtrain, 0, kD0, 1};
+                g.b = Opnd{c->slab + kOffW1, SW, kD0, 0};
+                g.c = c->act + kActH1; g.c_stride = kActStride; g.ldc = kH;
+                g.bias = c->slab + kOffB1; g.bias_stride = SW;
+                g.M = c->d.max_batch; g.m_is_bs = 1; g.N = kH; g.K = kD0;
+            } else {
+                g.a = Opnd{c->act + kActDH1, kActStride, kH, 0};
+                g.b = Opnd{c->xtrain, 0, kD0, 1};
+                g.c = c->grad + kOffW1; g.c_stride = kPAlloc; g.ldc = kD0;
+                g.M = kH; g.N = kD0; g.K = c->d.max_batch; g.k_is_bs = 1;
+            }
+            auto launch = [&] {
+                if (kind == 2)
+                    gemm<0, 0, kEpiBiasRelu>(c, g, n, c->d.max_batch);
+                else
+                    gemm<1, 1, kEpiStore>(c, g, n, kH);
+            };
+            for (int w = 0; w < 3; ++w) launch();
+            cudaEventRecord(c->ev[6], c->stream);
+            for (int r = 0; r < reps; ++r) launch();
+            cudaEventRecord(c->ev[7], c->stream);
         } else {
             fail(SMX_ECONFIG, "unknown kernel kind");
         }
