@@ -49,6 +49,9 @@ struct smx_ctx {
     int device = 0;
     int S = 0, C = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // second branch of the lockstep (weight gradients)
+    cudaStream_t cur = nullptr;   // stream the GEMM / reduction helpers enqueue on
+    cudaEvent_t fj[4] = {};       // fork / join events of the lockstep branches
 
     float* slab = nullptr;      // S x 2 x PAlloc  (w | m)
     float* grad = nullptr;      // S x PAlloc
@@ -105,20 +108,31 @@ GemmArgs base_args(smx_ctx* c, const int* d_slots) {
     return a;
 }
 
+// Weight-gradient GEMMs (row-contiguous A: batch-major gradients) use the TS variant whose A
+// operand goes registers -> TMEM; the rest use the SS variant (both operands through smem).
 template <int AM, int BMODE, int EPI>
 void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
+    constexpr bool kTs = AM == 1;
     static bool configured = false;  // per instantiation (device-independent attribute)
     if (!configured) {
-        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tc::kSmem),
-           "tc smem attribute");
+        if (kTs)
+            ck(cudaFuncSetAttribute(tc3::gemm_tc_ts_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc3::kSmem),
+               "tc smem attribute");
+        else
+            ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::kSmem),
+               "tc smem attribute");
         configured = true;
     }
     if ((a.a.ld & 3) || (a.b.ld & 3))
         fail(SMX_ECONFIG, "tensor-core GEMM needs 16-byte aligned operand rows (ld % 4 == 0)");
     const int mt = (m_max + tc::kBM - 1) / tc::kBM;
     dim3 grid((a.N + tc::kBN - 1) / tc::kBN, mt, groups);
-    tc::gemm_tc_kernel<AM, BMODE, EPI><<<grid, tc::kThreads, tc::kSmem, c->stream>>>(a, tc::kBN);
+    if (kTs)
+        tc3::gemm_tc_ts_kernel<AM, BMODE, EPI><<<grid, tc3::kThreads, tc3::kSmem, c->cur>>>(a, tc3::kBN);
+    else
+        tc::gemm_tc_kernel<AM, BMODE, EPI><<<grid, tc::kThreads, tc::kSmem, c->cur>>>(a, tc::kBN);
     launch_check(c, "gemm_tc");
 }
 
@@ -131,17 +145,17 @@ void gemm(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
         return;
     }
     dim3 grid((a.N + kTN - 1) / kTN, (m_max + kTM - 1) / kTM, groups);
-    gemm_simt_kernel<AM, BMODE, EPI><<<grid, 256, 0, c->stream>>>(a);
+    gemm_simt_kernel<AM, BMODE, EPI><<<grid, 256, 0, c->cur>>>(a);
     launch_check(c, "gemm_simt");
 }
 
 // Bias gradient of one layer: db[n] = sum over the batch of dY[r][n].
 void colsum(smx_ctx* c, const StepCtx& sc, int groups, long long dy_off, int ld, int N, long long db_off) {
     if (c->d.gemm_mode == SMX_GEMM_TC)
-        colsum_fast_kernel<<<dim3((N + 31) / 32, groups), 256, 0, c->stream>>>(sc, c->act, kActStride, dy_off, ld, N,
-                                                                                c->grad, kPAlloc, db_off);
+        colsum_fast_kernel<<<dim3((N + 31) / 32, groups), 256, 0, c->cur>>>(sc, c->act, kActStride, dy_off, ld, N,
+                                                                             c->grad, kPAlloc, db_off);
     else
-        colsum_kernel<<<dim3((N + 127) / 128, groups), 128, 0, c->stream>>>(sc, c->act, kActStride, dy_off, ld, N,
+        colsum_kernel<<<dim3((N + 127) / 128, groups), 128, 0, c->cur>>>(sc, c->act, kActStride, dy_off, ld, N,
                                                                              c->grad, kPAlloc, db_off);
     launch_check(c, "colsum");
 }
@@ -187,7 +201,15 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
         // ---- loss
         loss_train_kernel<<<n, kMaxBatch, 0, c->stream>>>(sc, c->ytrain, c->d.n_train - 1, A, AS, c->loss);
         launch_check(c, "loss_train");
+        // The backward pass runs as two branches: input gradients (dgrad) on the main stream,
+        // weight / bias gradients on the side stream as soon as their inputs exist.
+        auto fork = [&](int i) {
+            ck(cudaEventRecord(c->fj[i], c->stream), "fork record");
+            ck(cudaStreamWaitEvent(c->side, c->fj[i], 0), "fork wait");
+        };
         // ---- layer 3 grads
+        fork(0);
+        c->cur = c->side;
         if (c->d.gemm_mode == SMX_GEMM_TC) {
             GemmArgs g = base_args(c, d_slots);  // gW3^T[k][c] = sum_r H2[r][k] dZ[r][c], stored transposed
             g.a = Opnd{A + kActH2, AS, kH, 0};
@@ -204,6 +226,7 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             gemm<1, 1, kEpiStore>(c, g, n, kCP);
         }
         colsum(c, sc, n, kActDZ, kCP, kCP, kOffB3);
+        c->cur = c->stream;
         {
             GemmArgs g = base_args(c, d_slots);  // dH2[r][k] = (H2>0) sum_c dZ[r][c] W3[c][k]
             g.a = Opnd{A + kActDZ, AS, kCP, 0};
@@ -214,6 +237,8 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             gemm<0, 1, kEpiMask>(c, g, n, mb);
         }
         // ---- layer 2 grads
+        fork(1);
+        c->cur = c->side;
         {
             GemmArgs g = base_args(c, d_slots);
             g.a = Opnd{A + kActDH2, AS, kH, 0};
@@ -223,6 +248,7 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             gemm<1, 1, kEpiStore>(c, g, n, kH);
         }
         colsum(c, sc, n, kActDH2, kH, kH, kOffB2);
+        c->cur = c->stream;
         {
             GemmArgs g = base_args(c, d_slots);
             g.a = Opnd{A + kActDH2, AS, kH, 0};
@@ -233,6 +259,8 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             gemm<0, 1, kEpiMask>(c, g, n, mb);
         }
         // ---- layer 1 grads
+        fork(2);
+        c->cur = c->side;
         {
             GemmArgs g = base_args(c, d_slots);
             g.a = Opnd{A + kActDH1, AS, kH, 0};
@@ -242,6 +270,9 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
             gemm<1, 1, kEpiStore>(c, g, n, kH);
         }
         colsum(c, sc, n, kActDH1, kH, kH, kOffB1);
+        ck(cudaEventRecord(c->fj[3], c->side), "join record");
+        ck(cudaStreamWaitEvent(c->stream, c->fj[3], 0), "join wait");
+        c->cur = c->stream;
     }
     // ---- K5 update + advance
     if (c->timing) cudaEventRecord(c->ev[2], c->stream);
@@ -380,6 +411,9 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         c->C = n_ckpts;
         try {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+            c->cur = c->stream;
+            for (auto& e : c->fj) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "fork event");
             const long long P2 = 2 * kPAlloc;
             ck(cudaMalloc(&c->slab, sizeof(float) * P2 * n_slots), "slab");
             ck(cudaMalloc(&c->grad, sizeof(float) * kPAlloc * n_slots), "grad");
@@ -428,6 +462,9 @@ int smx_close(smx_ctx* c) {
         if (b) cudaFree(b);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->fj)
+        if (e) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return SMX_OK;
