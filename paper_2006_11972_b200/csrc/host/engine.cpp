@@ -8,6 +8,7 @@
 #include <numeric>
 
 #include "smx.h"
+#include "stagemerge/partition.hpp"
 
 namespace stagemerge {
 
@@ -176,32 +177,10 @@ TimeUs Engine::est_us(NodeId n) const {
 }
 
 std::set<NodeId> Engine::owned_roots() const {
-    std::set<NodeId> own;
     const auto& roots = plan_->roots();
     if (opts_.world <= 1) return {roots.begin(), roots.end()};
-    // LPT over root subtrees by step extent (deterministic; every rank computes the same map)
-    std::vector<NodeId> fresh;
-    for (NodeId r : roots)
-        if (!root_owner_.count(r)) fresh.push_back(r);
-    if (!fresh.empty()) {
-        std::map<NodeId, StepCount> work;
-        for (const PlanNode& n : plan_->nodes()) {
-            StepCount hi = n.start_step;
-            for (const auto& e : n.requests) hi = std::max(hi, e.end);
-            for (NodeId c : n.children) hi = std::max(hi, plan_->node(c).start_step);
-            NodeId r = n.id;
-            while (plan_->node(r).parent) r = *plan_->node(r).parent;
-            work[r] += hi - n.start_step;
-        }
-        std::vector<StepCount> load(static_cast<std::size_t>(opts_.world), 0);
-        for (const auto& [r, o] : root_owner_) load[static_cast<std::size_t>(o)] += work[r];
-        std::stable_sort(fresh.begin(), fresh.end(), [&](NodeId a, NodeId b) { return work[a] > work[b]; });
-        for (NodeId r : fresh) {
-            const auto o = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-            root_owner_[r] = o;
-            load[static_cast<std::size_t>(o)] += work[r];
-        }
-    }
+    assign_roots(*plan_, opts_.world, root_owner_);  // deterministic: every rank computes the same map
+    std::set<NodeId> own;
     for (const auto& [r, o] : root_owner_)
         if (o == opts_.rank) own.insert(r);
     return own;
@@ -214,11 +193,8 @@ std::set<NodeId> Engine::blocked_nodes() const {
             for (std::size_t i = w->cur; i < w->a.stages.size(); ++i) running.insert(w->a.stages[i].node);
     if (opts_.world > 1) {
         const std::set<NodeId> own = owned_roots();
-        for (const PlanNode& n : plan_->nodes()) {
-            NodeId r = n.id;
-            while (plan_->node(r).parent) r = *plan_->node(r).parent;
-            if (!own.count(r)) running.insert(n.id);
-        }
+        for (const PlanNode& n : plan_->nodes())
+            if (!own.count(root_of(*plan_, n.id))) running.insert(n.id);
     }
     return running;
 }

@@ -7,6 +7,7 @@
 
 #include "json_codec.hpp"
 #include "stagemerge/hpseq.hpp"
+#include "stagemerge/partition.hpp"
 #include "stagemerge/plan.hpp"
 #include "stagemerge/scheduler.hpp"
 #include "stagemerge/stage_tree.hpp"
@@ -231,6 +232,15 @@ json run(const json& cmd) {
             out["roundtrip_signature"] = SearchPlan::from_json(plan.to_json()).signature();
         out["file_name"] = PlanStore::file_name(key);
         if (cmd.contains("tree")) out["tree"] = tree_json(plan, cmd.at("tree"));
+        if (cmd.contains("partition")) {
+            std::map<NodeId, int> owner;
+            assign_roots(plan, cmd.at("partition").get<int>(), owner);
+            json own = json::object();
+            for (const auto& [r, o] : owner) own[std::to_string(r)] = o;
+            json work = json::object();
+            for (const auto& [r, w] : root_work(plan)) work[std::to_string(r)] = w;
+            out["partition"] = {{"owner", own}, {"work", work}};
+        }
     } else {
         throw ConfigError("unknown op " + op);
     }
