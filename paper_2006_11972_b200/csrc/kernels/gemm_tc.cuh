@@ -334,8 +334,9 @@ constexpr int kBM = 128;
 constexpr int kBN = 128;                         // N tile (the last tile may be narrower)
 constexpr int kKC = 32;                          // K elements per pipeline chunk
 constexpr int kKQ = kKC / 4;                     // 16-byte k-quads per chunk
-constexpr int kThreads = 256;
-constexpr int kAK = kKC / 2;                     // A k-values per thread per chunk (two warps per lane quadrant)
+constexpr int kThreads = 512;
+constexpr int kParts = kThreads / 128;           // warps per TMEM lane quadrant
+constexpr int kAK = kKC / kParts;                // A k-values per thread per chunk
 // B raw (as copied) tile: K-contiguous rows of kKC k padded by 4 floats, or kKC k-rows of 128 (+4)
 constexpr int kRawLdK = kKC + 4;
 constexpr int kRawLdMN = kBN + 4;
@@ -343,7 +344,7 @@ constexpr int kRawTile = kBN * kRawLdK * 4;      // 18432 B >= kKC * kRawLdMN * 
 // B K-major canonical: (row r, k) at (k/4)*kLbo + (r/8)*128 + (r%8)*16 + (k%4)*4   (SBO = 128)
 constexpr int kLbo = kBN * 16 + 16;              // 2064: padding keeps the split pass conflict-free
 constexpr int kTile = kKQ * kLbo;                // 16512 per hi or lo
-constexpr int kSmem = 2 * kRawTile + 4 * kTile + 64;  // raw x2, (hi, lo) x2, barriers: ~102 KB
+constexpr int kSmem = 4 * kRawTile + 4 * kTile + 64;  // (raw A, raw B) x2, (B hi, B lo) x2, barriers: ~140 KB
 // TMEM columns: [0,128) accumulator, then per buffer b: A_hi at 128 + 64b, A_lo at 160 + 64b
 constexpr int kTmemCols = 256;
 
@@ -398,17 +399,27 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src, int valid_by
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid_bytes));
 }
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-            taddr),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]));
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
 }
 
-// This thread's A values of one chunk: row `row`, k in [k, k + kAK).
-// AM == 0: A(m,k) = g[m*ld + k] (16-byte loads along k); AM == 1: A(m,k) = g[k*ld + m]
-// (one float per k, coalesced across the warp's consecutive rows).
+// This thread's A values of one chunk from the raw (as copied) A tile: tile row `r`, chunk-local
+// k in [k, k + kAK).  Raw rows are padded so both read patterns are bank-conflict free.
+template <int AM>
+__device__ __forceinline__ void read_a(const char* raw, int r, int k, float* v) {
+    if (AM == 0) {
+#pragma unroll
+        for (int q = 0; q < kAK / 4; ++q) {
+            const float4 t = *reinterpret_cast<const float4*>(raw + (r * kRawLdK + k + 4 * q) * 4);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kAK; ++i) v[i] = *reinterpret_cast<const float*>(raw + ((k + i) * kRawLdMN + r) * 4);
+    }
+}
+
 template <int AM>
 __device__ __forceinline__ void load_a(const float* g, int ld, int row, int M, int k, int K, float* v) {
     if (row >= M) {
@@ -453,9 +464,11 @@ __device__ __forceinline__ void load_b(const float* g, int ld, int r0, int rows,
         }
     } else {
         const int quads = rows >> 2;
-        const int units = quads * kKC;  // (row-quad, k): a warp reads 512 contiguous bytes of one k
-        for (int u = threadIdx.x; u < units; u += kThreads) {
-            const int rq = u % quads, k = u / quads;
+        // (row-quad, k) with 32 row-quads per k (idle lanes when rows < 128): a warp reads 512
+        // contiguous bytes of one k; power-of-two index math
+        for (int u = threadIdx.x; u < 32 * kKC; u += kThreads) {
+            const int rq = u & 31, k = u >> 5;
+            if (rq >= quads) continue;
             const int row = r0 + rq * 4, kk = k0 + k;
             const int valid = kk < klim ? max(0, min(4, rlim - row)) : 0;
             cp16(raw + (k * kRawLdMN + rq * 4) * 4, valid ? g + (long long)kk * ld + row : g, valid * 4);
@@ -474,9 +487,9 @@ __device__ __forceinline__ void split4(float4 v, float4& h, float4& l) {
 template <int MN, bool EXACT>
 __device__ __forceinline__ void split_b(const char* raw, int rows, char* hi, char* lo) {
     if (MN == 0) {
-        const int units = rows * kKQ;  // consecutive threads: consecutive rows, same k-quad
-        for (int u = threadIdx.x; u < units; u += kThreads) {
-            const int r = u % rows, kq = u / rows;
+        for (int u = threadIdx.x; u < 128 * kKQ; u += kThreads) {  // consecutive threads: consecutive rows
+            const int r = u & 127, kq = u >> 7;
+            if (r >= rows) continue;
             const float4 v = *reinterpret_cast<const float4*>(raw + (r * kRawLdK + kq * 4) * 4);
             const uint32_t off = kq * kLbo + (r >> 3) * 128 + (r & 7) * 16;
             float4 h, l;
@@ -486,9 +499,9 @@ __device__ __forceinline__ void split_b(const char* raw, int rows, char* hi, cha
         }
     } else {
         const int quads = rows >> 2;
-        const int units = quads * kKQ;  // 4 rows x 4 k per thread, transposed in registers
-        for (int u = threadIdx.x; u < units; u += kThreads) {
-            const int rq = u % quads, kq = u / quads;
+        for (int u = threadIdx.x; u < 32 * kKQ; u += kThreads) {  // 4 rows x 4 k per thread, transposed
+            const int rq = u & 31, kq = u >> 5;
+            if (rq >= quads) continue;
             float4 c[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -524,12 +537,12 @@ using tc::kTcMask;
 using tc::kTcStoreT;
 
 template <int AM, int BMODE, int EPI>
-__global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int /*unused*/) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_ts_kernel(GemmArgs p, int /*unused*/) {
     extern __shared__ __align__(1024) char smem[];
-    char* raw = smem;                                  // 2 B raw tiles
-    char* hl = smem + 2 * kRawTile;                    // 2 x (B_hi, B_lo)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kRawTile + 4 * kTile);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * kRawTile + 4 * kTile + 32);
+    char* raw = smem;                                  // 2 x (A raw, B raw)
+    char* hl = smem + 4 * kRawTile;                    // 2 x (B_hi, B_lo)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4 * kRawTile + 4 * kTile);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 4 * kRawTile + 4 * kTile + 32);
 
     const int slot = p.slots[blockIdx.z];
     const int bs = (p.m_is_bs || p.k_is_bs) ? slot_bs(p, slot) : 0;
@@ -547,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int
     const float* A = opnd_ptr(p.a, slot, p.st, p.n_train_mask);
     const float* B = opnd_ptr(p.b, slot, p.st, p.n_train_mask);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int quad = warp & 3, khalf = warp >> 2;
+    const int quad = warp & 3, kpart = warp >> 2;
     const int arow = m0 + quad * 32 + lane;
 
     if (warp == 0) {
@@ -570,26 +583,26 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int
     const int nchunks = (K + kKC - 1) / kKC;
     auto issue_b = [&](int c) {
         const int b = c & 1;
+        load_b<AM, false>(A, p.a.ld, m0, kBM, M, c * kKC, K, raw_u32 + b * 2 * kRawTile, 0);
         if (b_direct)
             load_b<BMODE, true>(B, p.b.ld, n0, nt, nlim, c * kKC, K, 0, hl_u32 + b * 2 * kTile);
         else
-            load_b<BMODE, false>(B, p.b.ld, n0, nt, nlim, c * kKC, K, raw_u32 + b * kRawTile, 0);
+            load_b<BMODE, false>(B, p.b.ld, n0, nt, nlim, c * kKC, K, raw_u32 + b * 2 * kRawTile + kRawTile, 0);
     };
     issue_b(0);
     asm volatile("cp.async.commit_group;");
     if (nchunks > 1) issue_b(1);
     asm volatile("cp.async.commit_group;");
-    float a_cur[kAK], a_nxt[kAK];
-    load_a<AM>(A, p.a.ld, arow, M, khalf * kAK, K, a_cur);
+    float a_cur[kAK];
 
 #pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
         const int b = c & 1;
-        if (c + 1 < nchunks) load_a<AM>(A, p.a.ld, arow, M, (c + 1) * kKC + khalf * kAK, K, a_nxt);
         asm volatile("cp.async.wait_group 1;");
         if (c >= 2) mbar_wait(&bars[b], ((c - 2) >> 1) & 1);  // MMAs of chunk c-2 released buffer b
         __syncthreads();
-        // A: split in registers, write hi/lo into TMEM (lane = row, column = k)
+        // A: raw smem -> registers -> split -> TMEM (lane = row, column = k)
+        read_a<AM>(raw + b * 2 * kRawTile, quad * 32 + lane, kpart * kAK, a_cur);
         {
             float hi[kAK], lo[kAK];
 #pragma unroll
@@ -597,18 +610,18 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int
                 hi[i] = a_exact ? a_cur[i] : tf32_rna(a_cur[i]);
                 lo[i] = tf32_rna(__fsub_rn(a_cur[i], hi[i]));
             }
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + 128 + b * 64 + khalf * kAK;
-            tmem_st16(ta, hi);
-            if (!a_exact) tmem_st16(ta + 32, lo);
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + 128 + b * 64 + kpart * kAK;
+            tmem_st8(ta, hi);
+            if (!a_exact) tmem_st8(ta + 32, lo);
             asm volatile("tcgen05.wait::st.sync.aligned;");
         }
         // B: split the landed raw tile into hi/lo canonical tiles
         if (!b_direct) {
             char* h = hl + b * 2 * kTile;
             if (b_exact)
-                split_b<BMODE, true>(raw + b * kRawTile, nt, h, h + kTile);
+                split_b<BMODE, true>(raw + b * 2 * kRawTile + kRawTile, nt, h, h + kTile);
             else
-                split_b<BMODE, false>(raw + b * kRawTile, nt, h, h + kTile);
+                split_b<BMODE, false>(raw + b * 2 * kRawTile + kRawTile, nt, h, h + kTile);
         }
         asm volatile("fence.proxy.async.shared::cta;");
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -637,8 +650,6 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int
             }
             mma_commit(&bars[b]);
         }
-#pragma unroll
-        for (int i = 0; i < kAK; ++i) a_cur[i] = a_nxt[i];
     }
     const int last = nchunks - 1;
     mbar_wait(&bars[last & 1], (last >> 1) & 1);
@@ -646,45 +657,56 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_tc_ts_kernel(GemmArgs p, int
 
     // ---- epilogue: warp w reads TMEM lanes 32*(w%4).., column half w/4 of the tile
     const int m = arow;
-    const int cols = nt / 2;
+    const int cols = nt / kParts;  // multiple of 4
     float* C = p.c + p.c_stride * slot;
-    const float* bias = (EPI == kTcBiasRelu || EPI == kTcBias) ? p.bias + p.bias_stride * slot : nullptr;
     const float* mask = (EPI == kTcMask) ? p.mask + p.mask_stride * slot : nullptr;
-    for (int c0 = khalf * cols; c0 < (khalf + 1) * cols; c0 += 8) {
-        uint32_t v[8];
+    float* bias = reinterpret_cast<float*>(raw);  // the tile's bias slice, staged once in smem
+    if (EPI == kTcBiasRelu || EPI == kTcBias) {
+        const float* gb = p.bias + p.bias_stride * slot;
+        for (int j = threadIdx.x; j < nt; j += kThreads) bias[j] = n0 + j < N ? gb[n0 + j] : 0.0f;
+        __syncthreads();
+    }
+    for (int c0 = kpart * cols; c0 < (kpart + 1) * cols; c0 += 4) {
+        uint32_t v[4];
         const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                      : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
         if (m >= M) continue;
         const int nb = n0 + c0;
-        float x[8];
+        float x[4], mk[4] = {1.f, 1.f, 1.f, 1.f};
+        if (EPI == kTcMask) {
+            const float* mp = mask + (long long)m * p.ldmask + nb;
+            if (nb + 4 <= N && (p.ldmask & 3) == 0) {
+                const float4 t4 = __ldg(reinterpret_cast<const float4*>(mp));
+                mk[0] = t4.x; mk[1] = t4.y; mk[2] = t4.z; mk[3] = t4.w;
+            } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < 4; ++j) mk[j] = nb + j < N ? mp[j] : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
             x[j] = __uint_as_float(v[j]);
-            const int n = nb + j;
-            if (n >= N) continue;
             if (EPI == kTcBiasRelu) {
-                x[j] = __fadd_rn(x[j], bias[n]);
+                x[j] = __fadd_rn(x[j], bias[c0 + j]);
                 x[j] = x[j] > 0.0f ? x[j] : 0.0f;
             } else if (EPI == kTcBias) {
-                x[j] = __fadd_rn(x[j], bias[n]);
+                x[j] = __fadd_rn(x[j], bias[c0 + j]);
             } else if (EPI == kTcMask) {
-                x[j] = mask[(long long)m * p.ldmask + n] > 0.0f ? x[j] : 0.0f;
+                x[j] = mk[j] > 0.0f ? x[j] : 0.0f;
             }
         }
         if (EPI == kTcStoreT) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 4; ++j)
                 if (nb + j < N) C[(long long)(nb + j) * p.ldc + m] = x[j];
-        } else if (nb + 8 <= N && (p.ldc & 3) == 0) {
-            float4* dst = reinterpret_cast<float4*>(C + (long long)m * p.ldc + nb);
-            dst[0] = make_float4(x[0], x[1], x[2], x[3]);
-            dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+        } else if (nb + 4 <= N && (p.ldc & 3) == 0) {
+            *reinterpret_cast<float4*>(C + (long long)m * p.ldc + nb) = make_float4(x[0], x[1], x[2], x[3]);
         } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 4; ++j)
                 if (nb + j < N) C[(long long)m * p.ldc + nb + j] = x[j];
         }
     }

@@ -112,7 +112,7 @@ GemmArgs base_args(smx_ctx* c, const int* d_slots) {
 // operand goes registers -> TMEM; the rest use the SS variant (both operands through smem).
 template <int AM, int BMODE, int EPI>
 void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
-    constexpr bool kTs = AM == 1;
+    constexpr bool kTs = true;
     static bool configured = false;  // per instantiation (device-independent attribute)
     if (!configured) {
         if (kTs)
