@@ -128,16 +128,31 @@ def reduce_sum(x: float, world: int) -> float:
     return float(t.item())
 
 
-def workload(n_studies: int):
+WORKLOADS = {
+    # name: (study spec, tuned?, description)
+    "c3": ("c3_random", False, "C3 space x {n} studies (256 random trials x 2000 steps each, seeds 0..{n1}), "
+                               "MLP 784-256-256-10, merged plan, root subtrees partitioned over ranks"),
+    "c4_sha": ("c4_sha", True, "C4 SHA (eta 4, rungs 150/600/1200 steps, 448-trial grid), MLP 784-256-256-10, "
+                               "one study per rank (replicas)"),
+    "c4_asha": ("c4_asha", True, "C4 ASHA (eta 4, rungs 150/600/1200 steps, 448-trial grid, 128 in flight), "
+                                 "MLP 784-256-256-10, one study per rank (replicas)"),
+}
+
+
+def workload(name: str, n_studies: int):
+    """Study specs of a workload; sampler seeds 0..n-1 for the partitioned (untuned) ones."""
     from paper_2006_11972_b200 import host
 
-    base = json.loads(host.study_spec("c3_random"))
+    spec_name, tuned, desc = WORKLOADS[name]
+    base = json.loads(host.study_spec(spec_name))
+    if tuned:
+        return [json.dumps(base)], True, desc.format(n=n_studies, n1=n_studies - 1)
     specs = []
     for s in range(n_studies):
         sp = dict(base)
         sp["sampler"] = {**base["sampler"], "seed": s}
         specs.append(json.dumps(sp))
-    return specs
+    return specs, False, desc.format(n=n_studies, n1=n_studies - 1)
 
 
 def cuda_time(fn, world):
@@ -176,7 +191,8 @@ def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
             rows[:, c] = r["hps"][name]["values"] if name in r["hps"] else [0.1, 0.9, 0.0, 128][c]
         hp.append(rows)
     ds = ol.dataset()
-    slots = [ol.Slot(max_steps=2001) for _ in range(n)]
+    T = min(int(info["max_steps"]), 2000)
+    slots = [ol.Slot(max_steps=T + 1) for _ in range(n)]
     lib = ol.oracle()
     FP = ctypes.POINTER(ctypes.c_float)
     W = (FP * n)(*[ol.fp(s.w) for s in slots])
@@ -186,15 +202,15 @@ def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
     step = (ctypes.c_int64 * n)()
     off = (ctypes.c_int64 * n)()
     done, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < seconds and done < 2000:
+    while time.perf_counter() - t0 < seconds and done + 2 <= T:
         k = 2
-        rc = lib.orc_train_many(n, W, M, step, off, H, 2000, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
+        rc = lib.orc_train_many(n, W, M, step, off, H, T, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
         assert rc == 0
         done += k
     dt = time.perf_counter() - t0
     stage_steps = n * done
     return {"value": stage_steps / dt * trial_per_stage, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{stage_steps} stage-steps ({n} trials x {done} steps of C3, OpenMP over {cores} threads) in "
+            "sample": f"{stage_steps} stage-steps ({n} trials x {done} steps of {info['name']}, OpenMP over {cores} threads) in "
                       f"{dt:.1f}s = {stage_steps / dt:.1f} stage-steps/s, x{trial_per_stage:.3f} trial-steps per "
                       f"stage-step (the plan's merge ratio)"}
 
@@ -203,7 +219,7 @@ def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (oracle port of the executor on the same plan)."""
     if rank != 0:
         return
-    specs = workload(1)
+    specs, _, _ = workload("c3", 1)
     from paper_2006_11972_b200 import host
 
     info = host.expand_study(specs[0])
@@ -233,6 +249,8 @@ def main():
     ap.add_argument("--gemm", default=os.environ.get("SMX_BENCH_GEMM", "tc"), choices=["exact", "tc"])
     ap.add_argument("--slots", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-trial", action="store_true", help="skip the TRIAL-mode (unmerged) comparison run")
     args = ap.parse_args()
     rank, world, local = dist_init()
     if args.impl == "reference":
@@ -244,17 +262,24 @@ def main():
     from paper_2006_11972_b200 import host
 
     torch.cuda.set_device(local)
-    specs = workload(world)
+    specs, tuned, desc = workload(args.workload, world)
     info = host.expand_study(specs[0])
     gemm_mode = ex.GEMM_TC if args.gemm == "tc" else ex.GEMM_EXACT
+    part = {} if tuned else {"rank": rank, "world": world}  # tuned studies: one replica per rank
     eng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
-                                gemm_mode=gemm_mode, rank=rank, world=world, max_steps=2048)
+                                gemm_mode=gemm_mode, max_steps=2048, **part)
+
+    def submit_and_run(e):
+        if tuned:
+            e.run_tuned(specs)
+        else:
+            for s, sp in enumerate(specs):
+                e.submit_study(sp, s)
+            e.run()
 
     def one_study():
         eng.reset()
-        for s, sp in enumerate(specs):
-            eng.submit_study(sp, s)
-        eng.run()
+        submit_and_run(eng)
         return eng.stats()
 
     for _ in range(args.warmup):
@@ -286,9 +311,7 @@ def main():
     def one_e2e():
         eng.reset()
         eng.upload_dataset(*host_arrays)
-        for s, sp in enumerate(specs):
-            eng.submit_study(sp, s)
-        eng.run()
+        submit_and_run(eng)
         return eng.stats()
 
     one_e2e()
@@ -296,6 +319,29 @@ def main():
     e2e_value = reduce_sum(st_e["trial_steps"], world) * args.steps / te
     for p in pinned:
         lib.smx_host_free(p)
+    eng.upload_dataset(*[np.ascontiguousarray(a) for a in (ds.x, ds.y, ds.vx, ds.vy)])
+
+    # ---- GPU-second savings: the same studies unmerged (TRIAL mode: every trial on its own
+    # path) on the same executor, device-timed once after one warm-up run
+    savings = None
+    if not args.no_trial:
+        teng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
+                                     gemm_mode=gemm_mode, max_steps=2048, trial_mode=True, **part)
+
+        def one_trial():
+            teng.reset()
+            submit_and_run(teng)
+            return teng.stats()
+
+        one_trial()
+        tt, st_t = cuda_time(one_trial, world)
+        savings = {"stage_gpu_s": t / args.steps, "trial_gpu_s": tt, "ratio": tt / (t / args.steps),
+                   "trial_mode_stage_steps": reduce_sum(st_t["stage_steps"], world),
+                   "trial_mode_trial_steps": reduce_sum(st_t["trial_steps"], world),
+                   "executed_merge_rate": trial_steps / stage_steps,
+                   "note": "GPU-busy seconds TRIAL / STAGE on the same executor (SPEC.md:396-398: tracks the "
+                           "executed merge rate when per-step cost is uniform)"}
+        del teng
 
     # ---- per-kernel roofline: standalone CUDA-event timing of the dominant kernels on a fresh
     # 64-slot context of the same GPU (bs 128, the study's typical active set)
@@ -345,9 +391,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"C3 space x {world} studies (256 random trials x 2000 steps each, seeds 0..{world - 1}), "
-                                   "MLP 784-256-256-10, merged plan, root subtrees partitioned over ranks",
-                       "gemm": args.gemm, "slots_per_gpu": args.slots, "trials": 256 * world,
+            "config": {"workload": desc,
+                       "gemm": args.gemm, "slots_per_gpu": args.slots, "trials": len(info["trials"]) * len(specs),
                        "trial_steps": trial_steps, "unique_stage_steps": stage_steps,
                        "executed_merge_rate": trial_steps / stage_steps,
                        "flush": "inputs > L2: per-slot state 2.2 MB x 128 slots + 206 MB dataset"},
@@ -359,6 +404,7 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "engine_stats": st,
+            "gpu_seconds_savings": savings,
         }
         print(json.dumps(line), flush=True)
 

@@ -54,7 +54,8 @@ struct EngineStats {
     double wall_s = 0;            // host wall time spent inside run()
     std::int64_t locksteps = 0;   // grouped training launches (sum over GPUs)
     std::int64_t stage_steps = 0; // (slot, step) updates executed
-    std::int64_t trial_steps = 0; // sum of end steps of completed requests' subscribers
+    std::int64_t trial_steps = 0; // sum over trials of the furthest end step reported to them
+                                  // (the work TRIAL mode would do; extensions count once)
     std::int64_t saves = 0, loads = 0, inits = 0, peer_copies = 0, evals = 0, assignments = 0, spills = 0;
     std::int64_t kernel_launches = 0;
     std::int64_t h2d_bytes = 0, d2h_bytes = 0;
@@ -76,6 +77,7 @@ public:
 
     using CompletionFn = std::function<void(Engine&, const CompletedRequest&)>;
     void on_complete(CompletionFn fn) { on_complete_ = std::move(fn); }
+    const CompletionFn& completion_callback() const { return on_complete_; }
 
     /// Runs until no schedulable work remains.
     void run();
@@ -118,6 +120,8 @@ private:
     std::vector<std::unique_ptr<Worker>> workers_;
     std::map<TrialRef, std::pair<StepCount, NodeId>> trial_index_;  // trial -> (end, terminal node)
     std::map<TrialRef, TrialConfig> trial_cfg_;
+    std::map<TrialRef, StepCount> reached_;  // furthest end reported per trial
+    void credit(const TrialRef& t, StepCount end);
     CompletionFn on_complete_;
     EngineStats stats_;
     int next_assignment_ = 0;

@@ -6,6 +6,7 @@
 #include "json_codec.hpp"
 #include "stagemerge/engine.hpp"
 #include "stagemerge/study.hpp"
+#include "stagemerge/tuner.hpp"
 
 namespace py = pybind11;
 using namespace stagemerge;
@@ -90,6 +91,21 @@ void bind_engine(py::module_& m) {
                  });
              })
         .def("cancel", [](Engine& e, int study, int trial) { return e.cancel(TrialRef{study, trial}); })
+        .def("run_tuned",
+             [](Engine& e, const std::vector<std::string>& specs, int base) {
+                 py::gil_scoped_release nogil;
+                 return translate([&] {
+                     json out = json::array();
+                     for (const StudyOutcome& o : run_tuned_studies(e, specs, base)) {
+                         json tt = json::object();
+                         for (const auto& [t, s] : o.trained_to) tt[std::to_string(t)] = s;
+                         out.push_back({{"study", o.study}, {"winners", o.winners}, {"actions", o.actions},
+                                        {"trained_to", tt}, {"trial_steps", o.trial_steps}});
+                     }
+                     return out.dump();
+                 });
+             },
+             py::arg("specs"), py::arg("base_study") = 0)
         .def("run",
              [](Engine& e) {
                  py::gil_scoped_release nogil;
@@ -134,6 +150,41 @@ void bind_engine(py::module_& m) {
                  e.upload_dataset(reinterpret_cast<const float*>(x), reinterpret_cast<const std::int32_t*>(y),
                                   reinterpret_cast<const float*>(vx), reinterpret_cast<const std::int32_t*>(vy));
              });
+
+    // Pure tuner state machine (no engine): start() / on_result() -> action strings.
+    struct PyTuner {
+        std::unique_ptr<Tuner> t;
+    };
+    py::class_<PyTuner>(m, "Tuner")
+        .def(py::init([](const std::string& spec_json) {
+            return translate([&] {
+                const StudySpec spec = parse_study(spec_json);
+                const TunerParams p = parse_tuner(spec_json, spec);
+                return PyTuner{make_tuner(p, static_cast<int>(spec.trials.size()), spec.max_steps)};
+            });
+        }))
+        .def("start",
+             [](PyTuner& t) {
+                 std::vector<std::string> v;
+                 for (const auto& a : translate([&] { return t.t->start(); })) v.push_back(a.to_string());
+                 return v;
+             })
+        .def("on_result",
+             [](PyTuner& t, int trial, long long end, const std::map<std::string, double>& metrics) {
+                 std::vector<std::string> v;
+                 for (const auto& a : translate([&] { return t.t->on_result(trial, end, metrics); }))
+                     v.push_back(a.to_string());
+                 return v;
+             })
+        .def("done", [](PyTuner& t) { return t.t->done(); })
+        .def("winners", [](PyTuner& t) { return t.t->winners(); });
+    m.def("sha_rungs", [](const std::string& spec_json) {
+        return translate([&] {
+            const StudySpec spec = parse_study(spec_json);
+            const Rungs r = sha_rungs(parse_tuner(spec_json, spec), static_cast<int>(spec.trials.size()));
+            return std::make_pair(r.ends, r.survivors);
+        });
+    });
 
     m.def("expand_study", [](const std::string& spec_json) {
         return translate([&] {

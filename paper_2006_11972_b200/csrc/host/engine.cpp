@@ -109,6 +109,7 @@ void Engine::reset() {
     }
     trial_index_.clear();
     trial_cfg_.clear();
+    reached_.clear();
     spilled_.clear();
     root_owner_.clear();
     stats_ = EngineStats{};
@@ -141,8 +142,16 @@ InsertOutcome Engine::submit(const TrialRequest& in) {
     const TrialRef t{in.study, in.trial};
     trial_index_[t] = {req.config.total_steps, out.node};
     trial_cfg_[t] = in.config;
-    if (out.kind == InsertOutcome::Kind::kImmediate) stats_.trial_steps += req.config.total_steps;
+    if (out.kind == InsertOutcome::Kind::kImmediate) credit(t, req.config.total_steps);
     return out;
+}
+
+void Engine::credit(const TrialRef& t, StepCount end) {
+    StepCount& r = reached_[t];
+    if (end > r) {
+        stats_.trial_steps += end - r;
+        r = end;
+    }
 }
 
 bool Engine::cancel(const TrialRef& t) { return plan_->cancel_trial(t); }
@@ -364,7 +373,7 @@ void Engine::finish_stages(std::vector<Worker*>& done) {
         const Stage s = w->a.stages[w->cur];
         if (auto it = records.find(w->id); it != records.end()) {
             for (const CompletedRequest& c : plan_->record_metrics(s.node, s.end, it->second)) {
-                stats_.trial_steps += static_cast<std::int64_t>(c.subscribers.size()) * c.end;
+                for (const TrialRef& t : c.subscribers) credit(t, c.end);
                 if (on_complete_) on_complete_(*this, c);
             }
         }

@@ -33,6 +33,30 @@ def expand_study(spec: str) -> dict:
     return json.loads(_native.expand_study(spec))
 
 
+class Tuner:
+    """A tuner state machine on its own (no engine): start() / on_result() return the actions
+    ("SUBMIT t end", "EXTEND t end", "STOP t", "DONE a,b") the C++ tuner issues."""
+
+    def __init__(self, spec: str):
+        self._t = _native.Tuner(spec)
+
+    def start(self) -> list:
+        return self._t.start()
+
+    def on_result(self, trial: int, end: int, metrics: dict) -> list:
+        return self._t.on_result(trial, end, metrics)
+
+    def done(self) -> bool:
+        return self._t.done()
+
+    def winners(self) -> list:
+        return self._t.winners()
+
+
+def sha_rungs(spec: str):
+    return _native.sha_rungs(spec)
+
+
 class Engine:
     """The study engine: plan + stage trees + scheduler (C++) driving the B200 executor."""
 
@@ -56,6 +80,13 @@ class Engine:
 
     def cancel(self, study: int, trial: int) -> bool:
         return self._e.cancel(study, trial)
+
+    def run_tuned(self, specs, base_study: int = 0) -> list:
+        """Runs every study spec under its own tuner (spec key "tuner") until each is DONE;
+        returns per study {study, winners, actions, trained_to, trial_steps}."""
+        if isinstance(specs, str):
+            specs = [specs]
+        return json.loads(self._e.run_tuned(list(specs), base_study))
 
     def run(self) -> None:
         self._e.run()
