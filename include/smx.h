@@ -55,6 +55,8 @@ extern "C" {
 #define SMX_EDEVICE 3
 
 #define SMX_MODEL_MLP 0 /* 784-256-256-10, ReLU, softmax-CE */
+#define SMX_MODEL_CNN 1 /* 3x32x32: conv3x3 3->32 s1, 32->64 s2, 64->128 s2, ReLU, GAP, FC 128->10
+                           (DESIGN.md §3b); inputs NHWC 32x32x4 (channel 3 = 0) */
 
 #define SMX_GEMM_EXACT 0 /* SIMT fp32, fixed fmaf order: bit-exact with the CPU oracle */
 #define SMX_GEMM_TC 1    /* tcgen05 kind::tf32, 3xTF32 split: fp32-level accuracy */
@@ -104,8 +106,9 @@ int smx_close(smx_ctx* ctx);
 int smx_param_count(const smx_ctx* ctx, int64_t* p, int64_t* p_alloc);
 /* FNV-1a over the bytes of the training/validation sets and labels. */
 int smx_dataset_digest(smx_ctx* ctx, uint64_t* out);
-/* Replace the synthetic dataset with host data: x (n_train + max_batch) x 784 fp32 (rows past
- * n_train repeat the first max_batch rows), y int32 labels, vx n_val x 784, vy.  Host->device
+/* Replace the synthetic dataset with host data: x (n_train + max_batch) x d_in fp32 (rows past
+ * n_train repeat the first max_batch rows; d_in = 784 for the MLP, 4096 = 32x32x4 for the CNN),
+ * y int32 labels, vx n_val x d_in, vy.  Host->device
  * copies on the context stream; pinned buffers (smx_host_alloc) make them DMA-direct. */
 int smx_dataset_upload(smx_ctx* ctx, const float* x, const int32_t* y, const float* vx, const int32_t* vy);
 /* Page-locked host buffers for the e2e path. */
@@ -146,7 +149,9 @@ int smx_get_stats(smx_ctx* ctx, smx_stats* out);
 int smx_reset_stats(smx_ctx* ctx);
 /* Standalone launches of one kernel class for roofline measurement: kind 0 = K5 update over
  * `n` slots, 1 = K6 fork copy of `n` checkpoints, 2 = the layer-1 forward GEMM over `n` slots,
- * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size).
+ * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size);
+ * for the CNN, 2 = the conv2 forward implicit GEMM and 3 = the conv2 weight gradient (split GEMM +
+ * ordered reduction).
  * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
 

@@ -133,6 +133,7 @@ private:
     std::map<CkptHandle, HostCkpt> spilled_;  // host spill tier of the checkpoint pool
     std::uint64_t use_clock_ = 0;
     std::int64_t p_alloc_ = 0;
+    std::int64_t d_in_ = 784;  // floats per input sample of the model
 };
 
 }  // namespace stagemerge

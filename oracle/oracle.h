@@ -35,4 +35,22 @@ int orc_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t* of
                    int threads);
 void orc_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out /* val_loss, val_acc */);
 
+/* softmax-CE of one row of 10 logits (shared by both models) */
+float orc_ce_row(const float* z, int y, float* dz, int* am);
+
+/* ---- CNN model (oracle/cnn.c) ---------------------------------------- */
+void orc_cnn_layout(int64_t* p_algo, int64_t* p_alloc, int64_t* off /* 9: W1 b1 W2 b2 W3 b3 W4 b4 end */);
+void orc_cnn_gen_dataset(uint64_t seed, int n_train, int max_batch, int n_val, float* x, int32_t* y, float* vx,
+                         int32_t* vy);
+void orc_cnn_init(uint64_t seed, float* w, float* m);
+int orc_cnn_train(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows, int n_steps,
+                  const float* x, const int32_t* y, int n_train, float* loss_hist);
+int orc_cnn_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t* offset, const float** hp,
+                       int64_t hp_rows, int n_steps, const float* x, const int32_t* y, int n_train, float** loss_hist,
+                       int threads);
+void orc_cnn_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out);
+void orc_cnn_conv_fwd(int l, const float* in, int B, const float* w, float* out);
+void orc_cnn_conv_wgrad(int l, const float* in, const float* dy, int B, float* grad);
+void orc_cnn_conv_dgrad(int l, const float* dy, const float* w, const float* act, int B, float* dx);
+
 #endif

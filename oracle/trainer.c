@@ -119,6 +119,8 @@ static float ce_row(const float* z, int y, float* dz, int* am) {
     return orc_log(s) - (z[y] - mx);
 }
 
+float orc_ce_row(const float* z, int y, float* dz, int* am) { return ce_row(z, y, dz, am); }
+
 /* ---- data / init ----------------------------------------------- */
 static void gen_rows(uint64_t seed, uint64_t stream, long rows, long n, float* x, int32_t* y) {
     signed char T[D0][NC];

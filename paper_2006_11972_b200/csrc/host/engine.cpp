@@ -57,7 +57,11 @@ Engine::Engine(CompatKey key, EngineOptions opts) : key_(std::move(key)), opts_(
         std::sort(key_.hp_set.begin(), key_.hp_set.end());
     }
     plan_ = std::make_unique<SearchPlan>(key_);
-    smx_model_desc d{SMX_MODEL_MLP, opts_.max_batch, opts_.n_train, opts_.n_val, opts_.max_steps, opts_.gemm_mode,
+    if (key_.model != "mlp" && key_.model != "cnn")
+        throw ConfigError("executor has no model '" + key_.model + "' (supported: mlp, cnn)");
+    const int model = key_.model == "cnn" ? SMX_MODEL_CNN : SMX_MODEL_MLP;
+    d_in_ = model == SMX_MODEL_CNN ? 32 * 32 * 4 : 784;
+    smx_model_desc d{model, opts_.max_batch, opts_.n_train, opts_.n_val, opts_.max_steps, opts_.gemm_mode,
                      opts_.seed};
     for (int dev : opts_.devices) {
         auto g = std::make_unique<Gpu>();
@@ -120,7 +124,7 @@ void Engine::upload_dataset(const float* x, const std::int32_t* y, const float* 
     for (auto& g : gpus_) smx_ok(smx_dataset_upload(g->ctx, x, y, vx, vy), "smx_dataset_upload");
     const std::int64_t rows = static_cast<std::int64_t>(opts_.n_train) + opts_.max_batch;
     stats_.h2d_bytes += static_cast<std::int64_t>(gpus_.size()) *
-                        (rows * 784 * 4 + rows * 4 + static_cast<std::int64_t>(opts_.n_val) * (784 * 4 + 4));
+                        (rows * d_in_ * 4 + rows * 4 + static_cast<std::int64_t>(opts_.n_val) * (d_in_ * 4 + 4));
 }
 
 std::uint64_t Engine::dataset_digest() {

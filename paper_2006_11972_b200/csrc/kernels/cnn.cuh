@@ -1,0 +1,755 @@
+// CNN model of the stage executor (SMX_MODEL_CNN, SURVEY §8d "small CNN"):
+//   conv3x3 3->32 s1 -> ReLU -> conv3x3 32->64 s2 -> ReLU -> conv3x3 64->128 s2 -> ReLU
+//   -> global average pool -> FC 128->10 -> softmax-CE;  PyTorch SGD (K5, shared with the MLP).
+//
+// Layout (HBM): images NHWC 32x32x4 (channel 3 == 0), activations NHWC per slot, conv weights
+// [Cout][kh*3+kw][Cin_pad].  Exact mode runs the SIMT kernels below (one thread per output, the
+// fmaf chain order of oracle/cnn.c); tensor-core mode runs every conv as an implicit GEMM on
+// tcgen05 (conv_tc_kernel): forward M = pixels, K = (tap, cin); input gradient per stride-2
+// parity class (dense taps only); weight gradient with the reduction over (sample, pixel) split
+// into fixed 2048-row ranges reduced in order by wgrad_reduce_kernel (deterministic, grouping
+// invariant) and the bias gradient as an extra all-ones row of the im2col operand.
+#pragma once
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "step_kernels.cuh"
+
+namespace smx {
+namespace cnn {
+
+constexpr int kImg = 32, kChReal = 3, kChPad = 4, kSample = kImg * kImg * kChPad;  // floats per image
+constexpr int kNC = 10, kNCP = 16, kFeat = 128;
+
+template <int L>
+struct Geo;
+template <>
+struct Geo<1> {
+    static constexpr int H = 32, Ci = 4, Cr = 3, Co = 32, S = 1, OH = 32;
+    static constexpr long long OffW = 0, OffB = 1152;
+};
+template <>
+struct Geo<2> {
+    static constexpr int H = 32, Ci = 32, Cr = 32, Co = 64, S = 2, OH = 16;
+    static constexpr long long OffW = 1184, OffB = 19616;
+};
+template <>
+struct Geo<3> {
+    static constexpr int H = 16, Ci = 64, Cr = 64, Co = 128, S = 2, OH = 8;
+    static constexpr long long OffW = 19680, OffB = 93408;
+};
+constexpr long long kOffW4 = 93536, kOffB4 = kOffW4 + kNCP * kFeat, kPEnd = kOffB4 + kNCP;
+constexpr long long kPAlloc = (kPEnd + 63) / 64 * 64;  // 95616
+constexpr long long kPAlgo = 32LL * 27 + 32 + 64LL * 288 + 64 + 128LL * 576 + 128 + 10LL * 128 + 10;  // 94538
+static_assert(Geo<1>::OffB == Geo<1>::OffW + 32 * 9 * 4 && Geo<2>::OffW == Geo<1>::OffB + 32, "layout");
+static_assert(Geo<2>::OffB == Geo<2>::OffW + 64 * 9 * 32 && Geo<3>::OffW == Geo<2>::OffB + 64, "layout");
+static_assert(Geo<3>::OffB == Geo<3>::OffW + 128 * 9 * 64 && kOffW4 == Geo<3>::OffB + 128, "layout");
+
+// weight-gradient split of the (sample, pixel) reduction: fixed 2048-row ranges
+constexpr int kSplitRows = 2048;
+template <int L>
+struct Part {
+    static constexpr int Rows = 9 * Geo<L>::Ci + 1;            // im2col rows + the all-ones (bias) row
+    static constexpr int Ld = (Rows + 3) / 4 * 4;               // floats per partial row
+    static constexpr int MaxSplit = (256 * Geo<L>::OH * Geo<L>::OH + kSplitRows - 1) / kSplitRows;
+    static constexpr long long Size = (long long)MaxSplit * Geo<L>::Co * Ld;
+};
+
+// Per-slot activation scratch: offsets in floats, tensors [max_batch][...] (computed on host).
+struct ActLayout {
+    long long a1, a2, a3, d1, d2, d3, g, z, dz, dg, rl, p1, p2, p3, stride;
+};
+inline ActLayout act_layout(int max_batch) {
+    ActLayout L{};
+    long long o = 0;
+    auto take = [&](long long per_sample) {
+        const long long at = o;
+        o += (per_sample * max_batch + 63) / 64 * 64;
+        return at;
+    };
+    L.a1 = take(1024 * 32);
+    L.a2 = take(256 * 64);
+    L.a3 = take(64 * 128);
+    L.d1 = take(1024 * 32);
+    L.d2 = take(256 * 64);
+    L.d3 = take(64 * 128);
+    L.g = take(kFeat);
+    L.z = take(kNCP);
+    L.dz = take(kNCP);
+    L.dg = take(kFeat);
+    L.rl = take(1);
+    L.p1 = o;
+    o += Part<1>::Size;
+    L.p2 = o;
+    o += Part<2>::Size;
+    L.p3 = o;
+    o += Part<3>::Size;
+    L.stride = (o + 63) / 64 * 64;
+    return L;
+}
+
+struct ConvArgs {
+    const int* slots;
+    const SlotState* st;
+    const float* hp;
+    int hp_cap;
+    int n_train_mask;
+    const float* x;      // image rows (train or validation set)
+    int x_from_slot;     // 1: first row = slot data offset (training); 0: x_row0 (eval chunk)
+    int x_row0;
+    int fixed_bs;        // > 0: batch size override (eval chunks)
+    float* slab;
+    long long slab_stride;
+    float* act;
+    ActLayout al;
+    float* grad;
+    long long grad_stride;
+    const int* labels;   // training labels (slot offset) or validation labels (x_row0)
+    float* loss_hist;
+    float* zout;         // eval: logits [group][n_val][16]
+    long long z_stride;
+};
+
+__device__ __forceinline__ int conv_bs(const ConvArgs& p, int slot) {
+    if (p.fixed_bs > 0) return p.fixed_bs;
+    return (int)p.hp[((long long)slot * p.hp_cap + p.st[slot].step) * 4 + 3];
+}
+__device__ __forceinline__ long long conv_row0(const ConvArgs& p, int slot) {
+    return p.x_from_slot ? (long long)(p.st[slot].offset & p.n_train_mask) : (long long)p.x_row0;
+}
+
+// ---- K8/K10 for images ----------------------------------------------------------------
+// x[r][h][w][c] = k/128, k = (hash(seed, stream, r mod n, (h*32+w)*3+c) & 0xFF) - 128; c = 3 -> 0.
+__global__ void gen_img_kernel(float* x, long long rows, int n, uint64_t seed, uint64_t stream) {
+    const long long total = rows * kSample;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / kSample;
+        const int e = (int)(i - r * kSample);
+        const int pix = e >> 2, ch = e & 3;
+        float v = 0.0f;
+        if (ch < kChReal) {
+            const uint64_t h = ckey(seed, stream, (uint64_t)(r % n), (uint64_t)(pix * kChReal + ch));
+            v = (float)((int)(h & 0xFF) - 128) * 0.0078125f;
+        }
+        x[i] = v;
+    }
+}
+
+// label = argmax_c sum_{h,w,ch} k * T[ch*16 + (h/8)*4 + w/8][c] (exact int32), ties -> smallest c.
+__global__ void gen_img_labels_kernel(const float* x, int* y, long long rows, uint64_t seed) {
+    __shared__ signed char T[kChReal * 16 * kNC];
+    for (int i = threadIdx.x; i < kChReal * 16 * kNC; i += blockDim.x) {
+        const int b = i / kNC, c = i % kNC;
+        T[i] = (signed char)((int)((ckey(seed, 7, (uint64_t)c, (uint64_t)b) >> 8) & 7) - 4);
+    }
+    __syncthreads();
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        int acc[kNC];
+#pragma unroll
+        for (int c = 0; c < kNC; ++c) acc[c] = 0;
+        const float* xr = x + r * kSample;
+        for (int pix = 0; pix < kImg * kImg; ++pix) {
+            const int h = pix >> 5, w = pix & 31;
+            for (int ch = 0; ch < kChReal; ++ch) {
+                const int k = (int)(xr[pix * 4 + ch] * 128.0f);
+                const int b = ch * 16 + (h >> 3) * 4 + (w >> 3);
+#pragma unroll
+                for (int c = 0; c < kNC; ++c) acc[c] += k * (int)T[b * kNC + c];
+            }
+        }
+        int best = 0;
+#pragma unroll
+        for (int c = 1; c < kNC; ++c)
+            if (acc[c] > acc[best]) best = c;
+        y[r] = best;
+    }
+}
+
+// He-uniform init (stream 8), identical for every root; padded entries stay 0.
+__global__ void cnn_init_kernel(float* w, float* m, uint64_t seed, float s1, float s2, float s3, float s4) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < kPAlloc;
+         i += (long long)gridDim.x * blockDim.x) {
+        int layer = 0, o = 0, in = 0;
+        float sc = 0.0f;
+        if (i < Geo<1>::OffB) {
+            const int r = (int)i;
+            o = r / 36; const int t = (r % 36) / 4, ci = r % 4;
+            if (ci < 3) { layer = 1; in = t * 3 + ci; sc = s1; }
+        } else if (i >= Geo<2>::OffW && i < Geo<2>::OffB) {
+            const int r = (int)(i - Geo<2>::OffW);
+            layer = 2; o = r / 288; in = r % 288; sc = s2;
+        } else if (i >= Geo<3>::OffW && i < Geo<3>::OffB) {
+            const int r = (int)(i - Geo<3>::OffW);
+            layer = 3; o = r / 576; in = r % 576; sc = s3;
+        } else if (i >= kOffW4 && i < kOffW4 + (long long)kNC * kFeat) {
+            const int r = (int)(i - kOffW4);
+            layer = 4; o = r / kFeat; in = r % kFeat; sc = s4;
+        }
+        float v = 0.0f;
+        if (layer) {
+            const uint64_t h = ckey(seed, 8, ((uint64_t)layer << 16) | (uint64_t)o, (uint64_t)in);
+            const int s = (int)((h >> 40) & 0xFFFFFF) - 8388608;
+            v = __fmul_rn((float)s, sc);
+        }
+        w[i] = v;
+        m[i] = 0.0f;
+    }
+}
+
+// ---- per-slot tensor addressing ---------------------------------------------------------
+struct SlotView {
+    int slot, bs;
+    const float* w;
+    float* act;
+};
+__device__ __forceinline__ SlotView slot_view(const ConvArgs& p, int slot) {
+    SlotView v;
+    v.slot = slot;
+    v.bs = conv_bs(p, slot);
+    v.w = p.slab + p.slab_stride * slot;
+    v.act = p.act + p.al.stride * slot;
+    return v;
+}
+template <int L>
+__device__ __forceinline__ const float* layer_in(const ConvArgs& p, const SlotView& v) {
+    if (L == 1) return p.x + conv_row0(p, v.slot) * kSample;
+    return v.act + (L == 2 ? p.al.a1 : p.al.a2);
+}
+template <int L>
+__device__ __forceinline__ float* layer_out(const ConvArgs& p, const SlotView& v) {
+    return v.act + (L == 1 ? p.al.a1 : L == 2 ? p.al.a2 : p.al.a3);
+}
+template <int L>
+__device__ __forceinline__ float* layer_dout(const ConvArgs& p, const SlotView& v) {  // dL/d(out of L)
+    return v.act + (L == 1 ? p.al.d1 : L == 2 ? p.al.d2 : p.al.d3);
+}
+
+// ---- exact mode: SIMT convolutions in the oracle's order ---------------------------------
+// out[n][p][co] = relu(b[co] + sum_{t valid asc} sum_{ci < Cr asc} in * W[co][t][ci])
+template <int L>
+__global__ void __launch_bounds__(256) conv_fwd_simt(ConvArgs p) {
+    using G = Geo<L>;
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const long long total = (long long)v.bs * G::OH * G::OH * G::Co;
+    const float* in = layer_in<L>(p, v);
+    float* out = layer_out<L>(p, v);
+    const float* W = v.w + G::OffW;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int co = (int)(i % G::Co);
+        const long long m = i / G::Co;
+        const int n = (int)(m / (G::OH * G::OH)), pix = (int)(m % (G::OH * G::OH));
+        const int oh = pix / G::OH, ow = pix % G::OH;
+        float acc = 0.0f;
+        for (int t = 0; t < 9; ++t) {
+            const int ih = oh * G::S + t / 3 - 1, iw = ow * G::S + t % 3 - 1;
+            if (ih < 0 || ih >= G::H || iw < 0 || iw >= G::H) continue;
+            const float* xin = in + (((long long)n * G::H + ih) * G::H + iw) * G::Ci;
+            const float* wr = W + ((long long)co * 9 + t) * G::Ci;
+            for (int ci = 0; ci < G::Cr; ++ci) acc = __fmaf_rn(xin[ci], wr[ci], acc);
+        }
+        const float r = __fadd_rn(acc, v.w[G::OffB + co]);
+        out[m * G::Co + co] = r > 0.0f ? r : 0.0f;
+    }
+}
+
+// gW[co][t][ci] = sum_{n asc, p asc, valid} dy * in;  gb[co] = sum dy (sequential)
+template <int L>
+__global__ void __launch_bounds__(128) conv_wgrad_simt(ConvArgs p) {
+    using G = Geo<L>;
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nw = G::Co * 9 * G::Ci;
+    if (i >= nw + G::Co) return;
+    const float* in = layer_in<L>(p, v);
+    const float* dy = layer_dout<L>(p, v);
+    float* g = p.grad + p.grad_stride * v.slot;
+    const int npix = G::OH * G::OH;
+    if (i >= nw) {
+        const int co = i - nw;
+        float s = 0.0f;
+        for (long long m = 0; m < (long long)v.bs * npix; ++m) s = __fadd_rn(s, dy[m * G::Co + co]);
+        g[G::OffB + co] = s;
+        return;
+    }
+    const int co = i / (9 * G::Ci), t = (i / G::Ci) % 9, ci = i % G::Ci;
+    float acc = 0.0f;
+    if (ci < G::Cr) {
+        const int kh = t / 3, kw = t % 3;
+        for (int n = 0; n < v.bs; ++n)
+            for (int pix = 0; pix < npix; ++pix) {
+                const int oh = pix / G::OH, ow = pix % G::OH;
+                const int ih = oh * G::S + kh - 1, iw = ow * G::S + kw - 1;
+                if (ih < 0 || ih >= G::H || iw < 0 || iw >= G::H) continue;
+                acc = __fmaf_rn(dy[((long long)n * npix + pix) * G::Co + co],
+                                in[(((long long)n * G::H + ih) * G::H + iw) * G::Ci + ci], acc);
+            }
+    }
+    g[G::OffW + i] = acc;
+}
+
+// dx[n][q][ci] = (act > 0) ? sum_{t asc valid} sum_{co asc} dy * W[co][t][ci] : 0
+template <int L>
+__global__ void __launch_bounds__(256) conv_dgrad_simt(ConvArgs p) {
+    using G = Geo<L>;
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const long long total = (long long)v.bs * G::H * G::H * G::Ci;
+    const float* dy = layer_dout<L>(p, v);
+    const float* act = layer_out<L - 1>(p, v);
+    float* dx = layer_dout<L - 1>(p, v);
+    const float* W = v.w + G::OffW;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int ci = (int)(i % G::Ci);
+        const long long q = i / G::Ci;
+        const int n = (int)(q / (G::H * G::H)), pix = (int)(q % (G::H * G::H));
+        const int ih = pix / G::H, iw = pix % G::H;
+        float acc = 0.0f;
+        for (int t = 0; t < 9; ++t) {
+            const int nh = ih + 1 - t / 3, nw = iw + 1 - t % 3;
+            if (nh < 0 || nw < 0 || nh % G::S || nw % G::S) continue;
+            const int oh = nh / G::S, ow = nw / G::S;
+            if (oh >= G::OH || ow >= G::OH) continue;
+            const float* d = dy + (((long long)n * G::OH + oh) * G::OH + ow) * G::Co;
+            const float* wr = W + (long long)t * G::Ci + ci;
+            for (int co = 0; co < G::Co; ++co) acc = __fmaf_rn(d[co], wr[(long long)co * 9 * G::Ci], acc);
+        }
+        dx[i] = act[i] > 0.0f ? acc : 0.0f;
+    }
+}
+
+// ---- head (both modes): pool + FC + softmax-CE, loss, FC grads, dA3 --------------------------
+// grid (max_batch, groups), block 128: one sample per block.
+// g[c] = (sum_{p asc} a3[p][c]) * 2^-6;  z[k] = fmaf chain over c of g[c]*W4[k][c], + b4[k]
+// train: dz = (softmax - onehot) / B, row loss;  eval (zout != null): logits to zout.
+__global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const int n = blockIdx.x;
+    if (n >= v.bs) return;
+    __shared__ float g[kFeat];
+    __shared__ float z[kNCP];
+    const int c = threadIdx.x;
+    const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
+    float s = 0.0f;
+    for (int pix = 0; pix < 64; ++pix) s = __fadd_rn(s, a3[pix * kFeat + c]);
+    g[c] = __fmul_rn(s, 0.015625f);
+    if (!p.zout) v.act[p.al.g + (long long)n * kFeat + c] = g[c];
+    __syncthreads();
+    if (c < kNCP) {
+        const float* wr = v.w + kOffW4 + c * kFeat;
+        float acc = 0.0f;
+        for (int i = 0; i < kFeat; ++i) acc = __fmaf_rn(g[i], wr[i], acc);
+        z[c] = __fadd_rn(acc, v.w[kOffB4 + c]);
+        if (p.zout) p.zout[p.z_stride * blockIdx.y + ((long long)p.x_row0 + n) * kNCP + c] = z[c];
+    }
+    __syncthreads();
+    if (!p.zout && c == 0) {
+        const int y = p.labels[conv_row0(p, v.slot) + n];
+        float dz[kNC];
+        const float l = softmax_ce_row(z, y, dz, nullptr);
+        v.act[p.al.rl + n] = l;
+        float* dzo = v.act + p.al.dz + (long long)n * kNCP;
+        const float fb = (float)v.bs;
+        for (int k = 0; k < kNC; ++k) dzo[k] = __fdiv_rn(dz[k], fb);
+        for (int k = kNC; k < kNCP; ++k) dzo[k] = 0.0f;
+    }
+}
+
+// grid (groups), block 256: loss = (sum_n rl) / B; gW4[k][c] = fmaf chain over n; gb4[k] = sum_n dz
+__global__ void __launch_bounds__(256) head_grad_kernel(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.x]);
+    const float* dz = v.act + p.al.dz;
+    const float* g = v.act + p.al.g;
+    float* gr = p.grad + p.grad_stride * v.slot;
+    for (int i = threadIdx.x; i < kNCP * kFeat + kNCP; i += blockDim.x) {
+        if (i < kNCP * kFeat) {
+            const int k = i / kFeat, c = i % kFeat;
+            float acc = 0.0f;
+            for (int n = 0; n < v.bs; ++n) acc = __fmaf_rn(dz[n * kNCP + k], g[n * kFeat + c], acc);
+            gr[kOffW4 + i] = acc;
+        } else {
+            const int k = i - kNCP * kFeat;
+            float s = 0.0f;
+            for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, dz[n * kNCP + k]);
+            gr[kOffB4 + k] = s;
+        }
+    }
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, v.act[p.al.rl + n]);
+        p.loss_hist[(long long)v.slot * p.hp_cap + p.st[v.slot].step] = __fdiv_rn(s, (float)v.bs);
+    }
+}
+
+// grid (max_batch, groups), block 128: dg[c] = (fmaf chain over k < 16 of dz*W4[k][c]) * 2^-6;
+// d3[n][p][c] = (a3 > 0) ? dg[c] : 0
+__global__ void __launch_bounds__(128) head_dg_kernel(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const int n = blockIdx.x;
+    if (n >= v.bs) return;
+    const int c = threadIdx.x;
+    const float* dz = v.act + p.al.dz + (long long)n * kNCP;
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kNCP; ++k) acc = __fmaf_rn(dz[k], v.w[kOffW4 + k * kFeat + c], acc);
+    const float dg = __fmul_rn(acc, 0.015625f);
+    const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
+    float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
+    for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = a3[pix * kFeat + c] > 0.0f ? dg : 0.0f;
+}
+
+// ---- tensor-core mode: implicit-GEMM convolutions on tcgen05 ------------------------------
+// The core is the TS variant of gemm_tc.cuh (A: cp.async raw -> registers -> hi/lo split ->
+// TMEM; B: cp.async raw -> smem hi/lo split -> UMMA canonical layout; 3xTF32, one thread issues
+// the MMAs, mbarrier-released double buffers), with the operands gathered by implicit-GEMM
+// address functions instead of a leading dimension, and several M tiles per CTA processed as one
+// flattened chunk stream (the next tile's loads overlap the current tile's epilogue).
+namespace ctc {
+using namespace smx::tc3;
+
+enum { kEpiBiasRelu = 0, kEpiMask = 1, kEpiPartT = 2 };
+constexpr int kConvSmem = kSmem + 512;  // + the tile's bias slice
+
+// source of zero-filled 16-byte copies (cp.async reads 0 bytes from it)
+__device__ __align__(16) float kZero16[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+
+// Forward: C[m = (n, oh, ow)][co] = relu(b + sum_{k = (t, ci)} im2col(in)[m][k] W[co][k])
+template <int L>
+struct Fwd {
+    using G = Geo<L>;
+    static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false;
+    static constexpr int kOnesRow = -1, kPartLd = 0;
+    const float* in;
+    const float* w;
+    const float* bias;
+    float* out;
+    int M, N, K, kbeg, m0, split;
+    __device__ void setup(const ConvArgs& p, const SlotView& v, int tile_y) {
+        in = layer_in<L>(p, v);
+        w = v.w + G::OffW;
+        bias = v.w + G::OffB;
+        out = layer_out<L>(p, v);
+        M = v.bs * G::OH * G::OH;
+        N = G::Co;
+        K = 9 * G::Ci;
+        kbeg = 0;
+        split = 0;
+        (void)tile_y;
+    }
+    __device__ __forceinline__ const float* a_ptr(int m, int k) const {
+        const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
+        const int t = k / G::Ci, ci = k % G::Ci;
+        const int ih = (pix / G::OH) * G::S + t / 3 - 1, iw = (pix % G::OH) * G::S + t % 3 - 1;
+        if (ih < 0 || ih >= G::H || iw < 0 || iw >= G::H) return nullptr;
+        return in + (((long long)n * G::H + ih) * G::H + iw) * G::Ci + ci;
+    }
+    __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
+    __device__ __forceinline__ float* c_row(int m) const { return out + (long long)m * G::Co; }
+    __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
+};
+
+// Input gradient of a stride-2 layer for one parity class (ih % 2, iw % 2) = (pi, pj):
+// rows r = (n, a, b) -> input pixel (2a + pi, 2b + pj); K = (dense tap j of the class, co).
+template <int L>
+struct Dgrad {
+    using G = Geo<L>;
+    static_assert(G::S == 2, "parity decomposition is for stride 2");
+    static constexpr int AM = 0, BMODE = 1, EPI = kEpiMask;
+    static constexpr bool A_EXACT = false, B_EXACT = false;
+    static constexpr int kOnesRow = -1, kPartLd = 0;
+    static constexpr int HH = G::H / 2;
+    const float* dy;
+    const float* w;
+    const float* act;
+    float* dx;
+    int M, N, K, kbeg, m0, split;
+    int pi, pj, nkw;  // class, taps per row of the class
+    __device__ void setup(const ConvArgs& p, const SlotView& v, int cls) {
+        dy = layer_dout<L>(p, v);
+        w = v.w + G::OffW;
+        act = layer_out<L - 1>(p, v);
+        dx = layer_dout<L - 1>(p, v);
+        pi = cls >> 1;
+        pj = cls & 1;
+        const int nkh = pi ? 2 : 1;
+        nkw = pj ? 2 : 1;
+        M = v.bs * HH * HH;
+        N = G::Ci;
+        K = nkh * nkw * G::Co;
+        kbeg = 0;
+        split = 0;
+    }
+    __device__ __forceinline__ void tap(int j, int& kh, int& kw) const {
+        const int jh = j / nkw, jw = j % nkw;
+        kh = pi ? 2 * jh : 1;
+        kw = pj ? 2 * jw : 1;
+    }
+    __device__ __forceinline__ long long pix_off(int r) const {
+        const int n = r / (HH * HH), q = r % (HH * HH);
+        const int ih = 2 * (q / HH) + pi, iw = 2 * (q % HH) + pj;
+        return (((long long)n * G::H + ih) * G::H + iw) * G::Ci;
+    }
+    __device__ __forceinline__ const float* a_ptr(int r, int k) const {
+        const int n = r / (HH * HH), q = r % (HH * HH);
+        const int ih = 2 * (q / HH) + pi, iw = 2 * (q % HH) + pj;
+        int kh, kw;
+        tap(k / G::Co, kh, kw);
+        const int oh = (ih + 1 - kh) >> 1, ow = (iw + 1 - kw) >> 1;  // parity makes these exact
+        if (ih + 1 - kh < 0 || iw + 1 - kw < 0 || oh >= G::OH || ow >= G::OH) return nullptr;
+        return dy + (((long long)n * G::OH + oh) * G::OH + ow) * G::Co + k % G::Co;
+    }
+    // B(row = ci, k = (j, co)) = W[co][t(j)][ci]; 4 consecutive ci are contiguous
+    __device__ __forceinline__ const float* b_ptr(int ci, int k) const {
+        int kh, kw;
+        tap(k / G::Co, kh, kw);
+        return w + ((long long)(k % G::Co) * 9 + kh * 3 + kw) * G::Ci + ci;
+    }
+    __device__ __forceinline__ float* c_row(int r) const { return dx + pix_off(r); }
+    __device__ __forceinline__ const float* mask_row(int r) const { return act + pix_off(r); }
+};
+
+// Weight gradient, split s of the reduction: part[s][co][k] = sum_{m in split} im2col(in)[m][k] dy[m][co]
+// (k = 9*Ci is the all-ones row: the bias gradient).
+template <int L>
+struct Wgrad {
+    using G = Geo<L>;
+    static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false;
+    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld;
+    const float* in;
+    const float* dy;
+    float* part;
+    int M, N, K, kbeg, m0, split;
+    __device__ void setup(const ConvArgs& p, const SlotView& v, int s) {
+        in = layer_in<L>(p, v);
+        dy = layer_dout<L>(p, v);
+        part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3);
+        const int total = v.bs * G::OH * G::OH;
+        split = s;
+        kbeg = s * kSplitRows;
+        K = max(0, min(kSplitRows, total - kbeg));
+        M = Part<L>::Rows;
+        N = G::Co;
+    }
+    // A(row = (t, ci), reduction m): 4 consecutive ci contiguous
+    __device__ __forceinline__ const float* a_ptr(int row, int m) const {
+        const int t = row / G::Ci, ci = row % G::Ci;
+        const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
+        const int ih = (pix / G::OH) * G::S + t / 3 - 1, iw = (pix % G::OH) * G::S + t % 3 - 1;
+        if (ih < 0 || ih >= G::H || iw < 0 || iw >= G::H) return nullptr;
+        return in + (((long long)n * G::H + ih) * G::H + iw) * G::Ci + ci;
+    }
+    __device__ __forceinline__ const float* b_ptr(int co, int m) const { return dy + (long long)m * G::Co + co; }
+    __device__ __forceinline__ float* c_row(int) const { return nullptr; }
+    __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
+};
+
+// cp.async of one operand tile through an address functor (16-byte units, zero fill).
+// MN == 0: unit (row, k-quad) -> f(row, k) points at 4 consecutive k of `row`;
+// MN == 1: unit (row-quad, k) -> f(row, k) points at rows row..row+3 at reduction index k.
+template <int MN, class F>
+__device__ __forceinline__ void load_tile(const F& f, int r0, int rows, int rlim, int k0, int klim, uint32_t raw) {
+    if (MN == 0) {
+        for (int u = threadIdx.x; u < rows * kKQ; u += kThreads) {
+            const int r = u / kKQ, kq = u % kKQ;
+            const int row = r0 + r, k = k0 + kq * 4;
+            const float* src = (row < rlim && k < klim) ? f(row, k) : nullptr;
+            cp16(raw + (r * kRawLdK + kq * 4) * 4, src ? src : kZero16, src ? 16 : 0);
+        }
+    } else {
+        for (int u = threadIdx.x; u < 32 * kKC; u += kThreads) {
+            const int rq = u & 31, k = u >> 5;
+            if (rq * 4 >= rows) continue;
+            const int row = r0 + rq * 4, kk = k0 + k;
+            const float* src = (row < rlim && kk < klim) ? f(row, kk) : nullptr;
+            cp16(raw + (k * kRawLdMN + rq * 4) * 4, src ? src : kZero16, src ? 16 : 0);
+        }
+    }
+}
+
+// grid: (x = class / split index, y = tile group, z = group); each CTA runs `tiles` M tiles.
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int tiles) {
+    extern __shared__ __align__(1024) char smem[];
+    char* raw = smem;
+    char* hl = smem + 4 * kRawTile;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4 * kRawTile + 4 * kTile);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 4 * kRawTile + 4 * kTile + 32);
+    float* bias_s = reinterpret_cast<float*>(smem + 4 * kRawTile + 4 * kTile + 64);  // 128 floats
+
+    const SlotView v = slot_view(p, p.slots[blockIdx.z]);
+    Op op;
+    op.setup(p, v, blockIdx.x);
+    const int M = op.M, N = op.N, K = op.K;
+    const int tile0 = blockIdx.y * tiles;
+    const int ntiles = min(tiles, (M + kBM - 1) / kBM - tile0);
+    if (ntiles <= 0 || K <= 0) return;
+    const int nt = (N + 15) / 16 * 16;
+    const int nchunks = (K + kKC - 1) / kKC;
+    const int total = ntiles * nchunks;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int quad = warp & 3, kpart = warp >> 2;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if constexpr (Op::EPI == kEpiBiasRelu)
+        for (int j = threadIdx.x; j < nt; j += kThreads) bias_s[j] = j < N ? op.bias[j] : 0.0f;
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = idesc_tf32(nt);
+    const uint32_t raw_u32 = smem_u32(raw), hl_u32 = smem_u32(hl);
+    const int klim = op.kbeg + K;
+
+    auto fa = [&](int r, int k) { return op.a_ptr(r, k); };
+    auto fb = [&](int r, int k) { return op.b_ptr(r, k); };
+    auto issue = [&](int g) {
+        const int b = g & 1;
+        const int m0 = (tile0 + g / nchunks) * kBM, k0 = op.kbeg + (g % nchunks) * kKC;
+        const int arlim = Op::kOnesRow >= 0 ? Op::kOnesRow : M;
+        load_tile<Op::AM>(fa, m0, kBM, arlim, k0, klim, raw_u32 + b * 2 * kRawTile);
+        load_tile<Op::BMODE>(fb, 0, nt, N, k0, klim, raw_u32 + b * 2 * kRawTile + kRawTile);
+    };
+    issue(0);
+    asm volatile("cp.async.commit_group;");
+    if (total > 1) issue(1);
+    asm volatile("cp.async.commit_group;");
+    float a_cur[kAK];
+
+#pragma unroll 1
+    for (int g = 0; g < total; ++g) {
+        const int b = g & 1;
+        const int c = g % nchunks;
+        const int m0 = (tile0 + g / nchunks) * kBM;
+        const int k0 = op.kbeg + c * kKC;
+        asm volatile("cp.async.wait_group 1;");
+        if (g >= 2) mbar_wait(&bars[b], ((g - 2) >> 1) & 1);
+        __syncthreads();
+        read_a<Op::AM>(raw + b * 2 * kRawTile, quad * 32 + lane, kpart * kAK, a_cur);
+        if (Op::kOnesRow >= 0 && m0 + quad * 32 + lane == Op::kOnesRow) {
+#pragma unroll
+            for (int i = 0; i < kAK; ++i) a_cur[i] = (k0 + kpart * kAK + i < klim) ? 1.0f : 0.0f;
+        }
+        {
+            float hi[kAK], lo[kAK];
+#pragma unroll
+            for (int i = 0; i < kAK; ++i) {
+                hi[i] = Op::A_EXACT ? a_cur[i] : tf32_rna(a_cur[i]);
+                lo[i] = tf32_rna(__fsub_rn(a_cur[i], hi[i]));
+            }
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + 128 + b * 64 + kpart * kAK;
+            tmem_st8(ta, hi);
+            if (!Op::A_EXACT) tmem_st8(ta + 32, lo);
+            asm volatile("tcgen05.wait::st.sync.aligned;");
+        }
+        {
+            char* h = hl + b * 2 * kTile;
+            split_b<Op::BMODE, Op::B_EXACT>(raw + b * 2 * kRawTile + kRawTile, nt, h, h + kTile);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (g + 2 < total) issue(g + 2);
+        asm volatile("cp.async.commit_group;");
+        if (threadIdx.x == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t bhi = hl_u32 + b * 2 * kTile, blo = bhi + kTile;
+            const uint32_t ahi = tmem + 128 + b * 64, alo = ahi + 32;
+            const int ksteps = (min(kKC, klim - k0) + 7) / 8;
+#pragma unroll 1
+            for (int s = 0; s < ksteps; ++s) {
+                const uint32_t o = s * 2 * kLbo;
+                const uint64_t dbh = smem_desc(bhi + o, kLbo, 128), dbl = smem_desc(blo + o, kLbo, 128);
+                uint32_t acc = (c == 0 && s == 0) ? 0u : 1u;
+                if (!Op::A_EXACT) {
+                    mma_ts(tmem, alo + s * 8, dbh, idesc, acc);
+                    acc = 1u;
+                }
+                if (!Op::B_EXACT) {
+                    mma_ts(tmem, ahi + s * 8, dbl, idesc, acc);
+                    acc = 1u;
+                }
+                mma_ts(tmem, ahi + s * 8, dbh, idesc, acc);
+            }
+            mma_commit(&bars[b]);
+        }
+        if (c != nchunks - 1) continue;
+
+        // ---- epilogue of this tile (the next tile's loads are already in flight)
+        mbar_wait(&bars[b], (g >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int m = m0 + quad * 32 + lane;
+        const int cols = nt / kParts;
+        for (int c0 = kpart * cols; c0 < (kpart + 1) * cols; c0 += 4) {
+            uint32_t r[4];
+            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (m >= M || c0 >= N) continue;
+            float x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j]);
+            if constexpr (Op::EPI == kEpiBiasRelu) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float t = __fadd_rn(x[j], bias_s[c0 + j]);
+                    x[j] = t > 0.0f ? t : 0.0f;
+                }
+                *reinterpret_cast<float4*>(op.c_row(m) + c0) = make_float4(x[0], x[1], x[2], x[3]);
+            } else if constexpr (Op::EPI == kEpiMask) {
+                const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_row(m) + c0));
+                *reinterpret_cast<float4*>(op.c_row(m) + c0) =
+                    make_float4(mk.x > 0.0f ? x[0] : 0.0f, mk.y > 0.0f ? x[1] : 0.0f, mk.z > 0.0f ? x[2] : 0.0f,
+                                mk.w > 0.0f ? x[3] : 0.0f);
+            } else {
+                float* pt = op.part + (long long)op.split * N * Op::kPartLd + m;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pt[(long long)(c0 + j) * Op::kPartLd] = x[j];
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+}  // namespace ctc
+
+// Weight-gradient reduction: grad[W][co][k] = sum_{s asc} part[s][co][k] (k < 9 Ci), grad[b][co]
+// from the all-ones row.  grid (Co, groups), block 128.
+template <int L>
+__global__ void __launch_bounds__(128) wgrad_reduce_kernel(ConvArgs p) {
+    using G = Geo<L>;
+    using P = Part<L>;
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const int co = blockIdx.x;
+    const int nsplit = (v.bs * G::OH * G::OH + kSplitRows - 1) / kSplitRows;
+    const float* part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3) + (long long)co * P::Ld;
+    float* g = p.grad + p.grad_stride * v.slot;
+    for (int k = threadIdx.x; k < P::Rows; k += blockDim.x) {
+        float s = 0.0f;
+        for (int i = 0; i < nsplit; ++i) s = __fadd_rn(s, part[(long long)i * G::Co * P::Ld + k]);
+        if (k < 9 * G::Ci)
+            g[G::OffW + (long long)co * 9 * G::Ci + k] = s;
+        else
+            g[G::OffB + co] = s;
+    }
+}
+
+}  // namespace cnn
+}  // namespace smx

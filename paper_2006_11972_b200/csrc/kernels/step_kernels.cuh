@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(StepCtx c, float* slab,
     const float* hp = hp_row(c, slot);
     const float nlr = -hp[0], mu = hp[1], wd = hp[2];
     float4* w = reinterpret_cast<float4*>(slab + slab_stride * slot);
-    float4* m = reinterpret_cast<float4*>(slab + slab_stride * slot + kPAlloc);
+    float4* m = reinterpret_cast<float4*>(slab + slab_stride * slot + slab_stride / 2);  // [w | m]
     const float4* g = reinterpret_cast<const float4*>(grad + grad_stride * slot);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
          i += (long long)gridDim.x * blockDim.x) {

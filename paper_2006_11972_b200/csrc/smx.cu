@@ -22,6 +22,7 @@
 #include "kernels/gemm_simt.cuh"
 #include "kernels/gemm_tc.cuh"
 #include "kernels/step_kernels.cuh"
+#include "kernels/cnn.cuh"
 
 using namespace smx;
 
@@ -60,7 +61,7 @@ struct smx_ctx {
     SlotState* ck_st = nullptr; // C
     float* hp = nullptr;        // S x cap x 4
     float* loss = nullptr;      // S x cap
-    float* act = nullptr;       // S x kActStride
+    float* act = nullptr;       // S x act_stride
     float* xtrain = nullptr;    // (n_train + max_batch) x 784
     int* ytrain = nullptr;
     float* xval = nullptr;      // n_val x 784
@@ -84,7 +85,16 @@ struct smx_ctx {
     smx_stats stats{};
     cudaEvent_t ev[8] = {};
 
-    long long slab_stride() const { return 2 * kPAlloc; }
+    // model geometry (MLP: common.cuh constants; CNN: cnn.cuh)
+    bool cnn = false;
+    long long palloc = kPAlloc;      // floats per parameter vector
+    long long act_stride = kActStride;
+    long long d_in = kD0;            // floats per input sample
+    cnn::ActLayout al{};
+    int lockstep_launches = 14;      // kernels per captured lockstep
+    float* zval = nullptr;           // CNN eval logits [kEvalChunk][n_val][16]
+
+    long long slab_stride() const { return 2 * palloc; }
 };
 
 namespace {
@@ -160,8 +170,175 @@ void colsum(smx_ctx* c, const StepCtx& sc, int groups, long long dy_off, int ld,
     launch_check(c, "colsum");
 }
 
+// ---- CNN (SMX_MODEL_CNN) -------------------------------------------------------------
+cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
+    cnn::ConvArgs a{};
+    a.slots = d_slots;
+    a.st = c->st;
+    a.hp = c->hp;
+    a.hp_cap = c->d.max_steps;
+    a.n_train_mask = c->d.n_train - 1;
+    a.x = c->xtrain;
+    a.x_from_slot = 1;
+    a.slab = c->slab;
+    a.slab_stride = c->slab_stride();
+    a.act = c->act;
+    a.al = c->al;
+    a.grad = c->grad;
+    a.grad_stride = c->palloc;
+    a.labels = c->ytrain;
+    a.loss_hist = c->loss;
+    return a;
+}
+
+// tiles per CTA of each tensor-core conv (amortises the CTA prologue over several M tiles)
+template <class Op>
+constexpr int conv_tpc() {
+    return 1;
+}
+template <>
+constexpr int conv_tpc<cnn::ctc::Fwd<1>>() { return 8; }
+template <>
+constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 2; }
+template <>
+constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 4; }
+template <>
+constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 2; }
+
+template <class Op>
+void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
+    static bool configured = false;
+    if (!configured) {
+        ck(cudaFuncSetAttribute(cnn::ctc::conv_tc_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cnn::ctc::kConvSmem),
+           "conv smem attribute");
+        configured = true;
+    }
+    constexpr int tpc = conv_tpc<Op>();
+    const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
+    dim3 grid(gx, (mtiles + tpc - 1) / tpc, groups);
+    cnn::ctc::conv_tc_kernel<Op><<<grid, tc3::kThreads, cnn::ctc::kConvSmem, c->cur>>>(a, tpc);
+    launch_check(c, "conv_tc");
+}
+
+template <int L>
+void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
+    using G = cnn::Geo<L>;
+    if (c->d.gemm_mode == SMX_GEMM_TC) {
+        conv_tc<cnn::ctc::Fwd<L>>(c, a, 1, mb * G::OH * G::OH, n);
+        return;
+    }
+    const long long total = (long long)mb * G::OH * G::OH * G::Co;
+    cnn::conv_fwd_simt<L><<<dim3((unsigned)std::min<long long>((total + 255) / 256, 1024), n), 256, 0, c->cur>>>(a);
+    launch_check(c, "conv_fwd_simt");
+}
+
+template <int L>
+void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
+    using G = cnn::Geo<L>;
+    if (c->d.gemm_mode == SMX_GEMM_TC) {
+        const int splits = (mb * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
+        conv_tc<cnn::ctc::Wgrad<L>>(c, a, splits, cnn::Part<L>::Rows, n);
+        cnn::wgrad_reduce_kernel<L><<<dim3(G::Co, n), 128, 0, c->cur>>>(a);
+        launch_check(c, "wgrad_reduce");
+        return;
+    }
+    cnn::conv_wgrad_simt<L><<<dim3((G::Co * 9 * G::Ci + G::Co + 127) / 128, n), 128, 0, c->cur>>>(a);
+    launch_check(c, "conv_wgrad_simt");
+}
+
+template <int L>
+void conv_dgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
+    using G = cnn::Geo<L>;
+    if (c->d.gemm_mode == SMX_GEMM_TC) {
+        conv_tc<cnn::ctc::Dgrad<L>>(c, a, 4, mb * (G::H / 2) * (G::H / 2), n);
+        return;
+    }
+    const long long total = (long long)mb * G::H * G::H * G::Ci;
+    cnn::conv_dgrad_simt<L><<<dim3((unsigned)std::min<long long>((total + 255) / 256, 1024), n), 256, 0, c->cur>>>(a);
+    launch_check(c, "conv_dgrad_simt");
+}
+
+// One lockstep of the CNN over `n` slots: forward, head, backward as two branches (input
+// gradients on the main stream, weight gradients on the side stream), K5 update, advance.
+void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
+    const int mb = c->d.max_batch;
+    const cnn::ConvArgs a = cnn_args(c, d_slots);
+    StepCtx sc = step_ctx(c, d_slots);
+    c->cur = c->stream;
+    conv_forward<1>(c, a, n, mb);
+    conv_forward<2>(c, a, n, mb);
+    conv_forward<3>(c, a, n, mb);
+    cnn::head_fwd_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
+    launch_check(c, "head_fwd");
+    cnn::head_grad_kernel<<<n, 256, 0, c->stream>>>(a);
+    launch_check(c, "head_grad");
+    cnn::head_dg_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
+    launch_check(c, "head_dg");
+    auto fork = [&](int i) {
+        ck(cudaEventRecord(c->fj[i], c->stream), "fork record");
+        ck(cudaStreamWaitEvent(c->side, c->fj[i], 0), "fork wait");
+    };
+    fork(0);
+    c->cur = c->side;
+    conv_wgrad<3>(c, a, n, mb);
+    c->cur = c->stream;
+    conv_dgrad<3>(c, a, n, mb);
+    fork(1);
+    c->cur = c->side;
+    conv_wgrad<2>(c, a, n, mb);
+    c->cur = c->stream;
+    conv_dgrad<2>(c, a, n, mb);
+    fork(2);
+    c->cur = c->side;
+    conv_wgrad<1>(c, a, n, mb);
+    ck(cudaEventRecord(c->fj[3], c->side), "join record");
+    ck(cudaStreamWaitEvent(c->stream, c->fj[3], 0), "join wait");
+    c->cur = c->stream;
+    if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+    {
+        const long long n4 = c->palloc / 4;
+        const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
+        sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, c->palloc, n4);
+        launch_check(c, "sgd_update");
+    }
+    if (c->timing) cudaEventRecord(c->ev[3], c->stream);
+    advance_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(sc, n);
+    launch_check(c, "advance");
+}
+
+// Validation metrics of k slots (device list eval_slots): forward in chunks of max_batch
+// samples through the slots' own activation buffers, logits to zval, then the shared
+// fixed-order reduction (eval_reduce_kernel).
+void eval_cnn(smx_ctx* c, int k) {
+    const int mb = c->d.max_batch, nv = c->d.n_val;
+    cnn::ConvArgs a = cnn_args(c, c->eval_slots);
+    a.x = c->xval;
+    a.x_from_slot = 0;
+    a.fixed_bs = mb;
+    a.labels = c->yval;
+    a.zout = c->zval;
+    a.z_stride = (long long)nv * cnn::kNCP;
+    c->cur = c->stream;
+    for (int r0 = 0; r0 < nv; r0 += mb) {
+        a.x_row0 = r0;
+        conv_forward<1>(c, a, k, mb);
+        conv_forward<2>(c, a, k, mb);
+        conv_forward<3>(c, a, k, mb);
+        cnn::head_fwd_kernel<<<dim3(mb, k), 128, 0, c->stream>>>(a);
+        launch_check(c, "head_fwd eval");
+    }
+    eval_reduce_kernel<<<k, 256, 0, c->stream>>>(c->eval_slots, c->zval, a.z_stride, c->yval, nv, c->eval_scratch,
+                                                 c->eval_out);
+    launch_check(c, "eval_reduce");
+}
+
 // One lockstep of the MLP over `n` slots listed in device array d_slots.
 void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
+    if (c->cnn) {
+        enqueue_lockstep_cnn(c, d_slots, n);
+        return;
+    }
     const int mb = c->d.max_batch;
     const long long SW = c->slab_stride(), AS = kActStride;
     float* W = c->slab;
@@ -322,6 +499,17 @@ smx_ctx::Graph& graph_for(smx_ctx* c, const std::vector<int>& slots) {
 
 void gen_dataset(smx_ctx* c) {
     const long long rows = (long long)c->d.n_train + c->d.max_batch;
+    if (c->cnn) {
+        cnn::gen_img_kernel<<<1184, 256, 0, c->stream>>>(c->xtrain, rows, c->d.n_train, c->d.seed, 5);
+        launch_check(c, "gen_img train");
+        cnn::gen_img_labels_kernel<<<296, 128, 0, c->stream>>>(c->xtrain, c->ytrain, rows, c->d.seed);
+        launch_check(c, "gen_img_labels train");
+        cnn::gen_img_kernel<<<1184, 256, 0, c->stream>>>(c->xval, c->d.n_val, c->d.n_val, c->d.seed, 6);
+        launch_check(c, "gen_img val");
+        cnn::gen_img_labels_kernel<<<296, 128, 0, c->stream>>>(c->xval, c->yval, c->d.n_val, c->d.seed);
+        launch_check(c, "gen_img_labels val");
+        return;
+    }
     gen_x_kernel<<<1184, 256, 0, c->stream>>>(c->xtrain, rows, c->d.n_train, c->d.seed, kStreamTrain);
     launch_check(c, "gen_x train");
     gen_labels_kernel<<<296, 128, 0, c->stream>>>(c->xtrain, c->ytrain, rows, c->d.seed);
@@ -353,7 +541,7 @@ void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
     }
     ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * jobs.size(), cudaMemcpyHostToDevice, c->stream),
        "jobs H2D");
-    const long long n4 = 2 * kPAlloc / 4;
+    const long long n4 = 2 * c->palloc / 4;
     if (c->timing) cudaEventRecord(c->ev[4], c->stream);
     fork_copy_kernel<<<dim3(148, (unsigned)jobs.size()), 256, 0, c->stream>>>(c->jobs, n4);
     launch_check(c, "fork_copy");
@@ -393,7 +581,8 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
     return guard([&] {
         if (!desc || !out) fail(SMX_ECONFIG, "null argument");
         const smx_model_desc& d = *desc;
-        if (d.model != SMX_MODEL_MLP) fail(SMX_ECONFIG, "unsupported model id " + std::to_string(d.model));
+        if (d.model != SMX_MODEL_MLP && d.model != SMX_MODEL_CNN)
+            fail(SMX_ECONFIG, "unsupported model id " + std::to_string(d.model));
         if (d.max_batch < 1 || d.max_batch > kMaxBatch) fail(SMX_ECONFIG, "max_batch must be in [1, 256]");
         if (d.n_train < 256 || (d.n_train & (d.n_train - 1))) fail(SMX_ECONFIG, "n_train must be a power of two >= 256");
         if (d.n_val < 128 || d.n_val % 128) fail(SMX_ECONFIG, "n_val must be a positive multiple of 128");
@@ -409,34 +598,47 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         c->device = device;
         c->S = n_slots;
         c->C = n_ckpts;
+        if (d.model == SMX_MODEL_CNN) {
+            if (d.n_val % d.max_batch) fail(SMX_ECONFIG, "CNN: n_val must be a multiple of max_batch");
+            c->cnn = true;
+            c->palloc = cnn::kPAlloc;
+            c->al = cnn::act_layout(d.max_batch);
+            c->act_stride = c->al.stride;
+            c->d_in = cnn::kSample;
+            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 16 : 13;
+        }
         try {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
             c->cur = c->stream;
             for (auto& e : c->fj) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "fork event");
-            const long long P2 = 2 * kPAlloc;
+            const long long P2 = 2 * c->palloc;
             ck(cudaMalloc(&c->slab, sizeof(float) * P2 * n_slots), "slab");
-            ck(cudaMalloc(&c->grad, sizeof(float) * kPAlloc * n_slots), "grad");
+            ck(cudaMalloc(&c->grad, sizeof(float) * c->palloc * n_slots), "grad");
             if (n_ckpts) ck(cudaMalloc(&c->pool, sizeof(float) * P2 * n_ckpts), "pool");
             ck(cudaMalloc(&c->st, sizeof(SlotState) * n_slots), "state");
             ck(cudaMalloc(&c->ck_st, sizeof(SlotState) * (n_ckpts ? n_ckpts : 1)), "ck state");
             ck(cudaMalloc(&c->hp, sizeof(float) * 4 * (long long)d.max_steps * n_slots), "hp");
             ck(cudaMalloc(&c->loss, sizeof(float) * (long long)d.max_steps * n_slots), "loss");
-            ck(cudaMalloc(&c->act, sizeof(float) * kActStride * n_slots), "act");
+            ck(cudaMalloc(&c->act, sizeof(float) * c->act_stride * n_slots), "act");
             const long long rows = (long long)d.n_train + d.max_batch;
-            ck(cudaMalloc(&c->xtrain, sizeof(float) * rows * kD0), "xtrain");
+            ck(cudaMalloc(&c->xtrain, sizeof(float) * rows * c->d_in), "xtrain");
             ck(cudaMalloc(&c->ytrain, sizeof(int) * rows), "ytrain");
-            ck(cudaMalloc(&c->xval, sizeof(float) * (long long)d.n_val * kD0), "xval");
+            ck(cudaMalloc(&c->xval, sizeof(float) * (long long)d.n_val * c->d_in), "xval");
             ck(cudaMalloc(&c->yval, sizeof(int) * d.n_val), "yval");
-            ck(cudaMalloc(&c->eval_act, sizeof(float) * kEvalChunk * (long long)d.n_val * (2 * kH + kCP)), "eval act");
+            if (c->cnn)
+                ck(cudaMalloc(&c->zval, sizeof(float) * kEvalChunk * (long long)d.n_val * cnn::kNCP), "eval logits");
+            else
+                ck(cudaMalloc(&c->eval_act, sizeof(float) * kEvalChunk * (long long)d.n_val * (2 * kH + kCP)),
+                   "eval act");
             ck(cudaMalloc(&c->eval_scratch, sizeof(float) * kEvalChunk * (long long)d.n_val), "eval scratch");
             ck(cudaMalloc(&c->eval_out, sizeof(double) * 2 * kEvalChunk), "eval out");
             ck(cudaMalloc(&c->eval_slots, sizeof(int) * kEvalChunk), "eval slots");
             ck(cudaMalloc(&c->scratch_slots, sizeof(int) * n_slots), "scratch slots");
-            ck(cudaMemsetAsync(c->grad, 0, sizeof(float) * kPAlloc * n_slots, c->stream), "grad zero");
+            ck(cudaMemsetAsync(c->grad, 0, sizeof(float) * c->palloc * n_slots, c->stream), "grad zero");
             ck(cudaMemsetAsync(c->hp, 0, sizeof(float) * 4 * (long long)d.max_steps * n_slots, c->stream), "hp zero");
             ck(cudaMemsetAsync(c->loss, 0, sizeof(float) * (long long)d.max_steps * n_slots, c->stream), "loss zero");
-            ck(cudaMemsetAsync(c->act, 0, sizeof(float) * kActStride * n_slots, c->stream), "act zero");
+            ck(cudaMemsetAsync(c->act, 0, sizeof(float) * c->act_stride * n_slots, c->stream), "act zero");
             ck(cudaMemsetAsync(c->st, 0, sizeof(SlotState) * n_slots, c->stream), "state zero");
             for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
             c->ck_valid.assign(n_ckpts, 0);
@@ -456,7 +658,7 @@ int smx_close(smx_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_graphs(c);
     void* bufs[] = {c->slab, c->grad, c->pool, c->st, c->ck_st, c->hp, c->loss, c->act, c->xtrain, c->ytrain,
-                    c->xval, c->yval, c->eval_act, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
+                    c->xval, c->yval, c->eval_act, c->zval, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
                     c->scratch_slots};
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -471,9 +673,10 @@ int smx_close(smx_ctx* c) {
 }
 
 int smx_param_count(const smx_ctx* c, int64_t* p, int64_t* p_alloc) {
-    (void)c;
-    if (p) *p = kPAlgo;
-    if (p_alloc) *p_alloc = kPAlloc;
+    // without a context: the MLP (the default model)
+    const bool cnn_model = c && c->cnn;
+    if (p) *p = cnn_model ? cnn::kPAlgo : kPAlgo;
+    if (p_alloc) *p_alloc = cnn_model ? cnn::kPAlloc : kPAlloc;
     return SMX_OK;
 }
 
@@ -481,9 +684,9 @@ int smx_dataset_digest(smx_ctx* c, uint64_t* out) {
     return guard([&] {
         cudaSetDevice(c->device);
         const long long rows = (long long)c->d.n_train + c->d.max_batch;
-        std::vector<float> x(rows * kD0);
+        std::vector<float> x(rows * c->d_in);
         std::vector<int> y(rows);
-        std::vector<float> vx((long long)c->d.n_val * kD0);
+        std::vector<float> vx((long long)c->d.n_val * c->d_in);
         std::vector<int> vy(c->d.n_val);
         ck(cudaMemcpyAsync(x.data(), c->xtrain, sizeof(float) * x.size(), cudaMemcpyDeviceToHost, c->stream), "x D2H");
         ck(cudaMemcpyAsync(y.data(), c->ytrain, sizeof(int) * y.size(), cudaMemcpyDeviceToHost, c->stream), "y D2H");
@@ -511,9 +714,9 @@ int smx_dataset_upload(smx_ctx* c, const float* x, const int32_t* y, const float
         if (!x || !y || !vx || !vy) fail(SMX_ECONFIG, "null dataset buffer");
         cudaSetDevice(c->device);
         const long long rows = (long long)c->d.n_train + c->d.max_batch;
-        ck(cudaMemcpyAsync(c->xtrain, x, sizeof(float) * rows * kD0, cudaMemcpyHostToDevice, c->stream), "x H2D");
+        ck(cudaMemcpyAsync(c->xtrain, x, sizeof(float) * rows * c->d_in, cudaMemcpyHostToDevice, c->stream), "x H2D");
         ck(cudaMemcpyAsync(c->ytrain, y, sizeof(int) * rows, cudaMemcpyHostToDevice, c->stream), "y H2D");
-        ck(cudaMemcpyAsync(c->xval, vx, sizeof(float) * (long long)c->d.n_val * kD0, cudaMemcpyHostToDevice, c->stream),
+        ck(cudaMemcpyAsync(c->xval, vx, sizeof(float) * (long long)c->d.n_val * c->d_in, cudaMemcpyHostToDevice, c->stream),
            "vx H2D");
         ck(cudaMemcpyAsync(c->yval, vy, sizeof(int) * c->d.n_val, cudaMemcpyHostToDevice, c->stream), "vy H2D");
         ck(cudaStreamSynchronize(c->stream), "dataset sync");
@@ -554,8 +757,12 @@ int smx_slot_init(smx_ctx* c, int slot) {
         check_slot(c, slot);
         cudaSetDevice(c->device);
         float* w = c->slab + c->slab_stride() * slot;
-        init_kernel<<<296, 256, 0, c->stream>>>(w, w + kPAlloc, c->d.seed, init_scale(kD0), init_scale(kH),
-                                                init_scale(kH));
+        if (c->cnn)
+            cnn::cnn_init_kernel<<<296, 256, 0, c->stream>>>(w, w + c->palloc, c->d.seed, init_scale(27), init_scale(288),
+                                                             init_scale(576), init_scale(128));
+        else
+            init_kernel<<<296, 256, 0, c->stream>>>(w, w + kPAlloc, c->d.seed, init_scale(kD0), init_scale(kH),
+                                                    init_scale(kH));
         launch_check(c, "init");
         ck(cudaMemsetAsync(c->st + slot, 0, sizeof(SlotState), c->stream), "state reset");
     });
@@ -647,8 +854,8 @@ int smx_slot_read(smx_ctx* c, int slot, float* w, float* m) {
         check_slot(c, slot);
         cudaSetDevice(c->device);
         const float* base = c->slab + c->slab_stride() * slot;
-        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
-        if (m) ck(cudaMemcpyAsync(m, base + kPAlloc, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
+        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * c->palloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
+        if (m) ck(cudaMemcpyAsync(m, base + c->palloc, sizeof(float) * c->palloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
         ck(cudaStreamSynchronize(c->stream), "read sync");
     });
 }
@@ -658,8 +865,8 @@ int smx_slot_write(smx_ctx* c, int slot, const float* w, const float* m, int64_t
         check_slot(c, slot);
         cudaSetDevice(c->device);
         float* base = c->slab + c->slab_stride() * slot;
-        ck(cudaMemcpyAsync(base, w, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
-        ck(cudaMemcpyAsync(base + kPAlloc, m, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
+        ck(cudaMemcpyAsync(base, w, sizeof(float) * c->palloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
+        ck(cudaMemcpyAsync(base + c->palloc, m, sizeof(float) * c->palloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
         SlotState s{step, offset};
         ck(cudaMemcpyAsync(c->st + slot, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state H2D");
         ck(cudaStreamSynchronize(c->stream), "write sync");
@@ -673,8 +880,8 @@ int smx_ckpt_read(smx_ctx* c, int ckpt, float* w, float* m, int64_t* step, int64
         cudaSetDevice(c->device);
         const float* base = c->pool + c->slab_stride() * ckpt;
         SlotState s;
-        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
-        if (m) ck(cudaMemcpyAsync(m, base + kPAlloc, sizeof(float) * kPAlloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
+        if (w) ck(cudaMemcpyAsync(w, base, sizeof(float) * c->palloc, cudaMemcpyDeviceToHost, c->stream), "w D2H");
+        if (m) ck(cudaMemcpyAsync(m, base + c->palloc, sizeof(float) * c->palloc, cudaMemcpyDeviceToHost, c->stream), "m D2H");
         ck(cudaMemcpyAsync(&s, c->ck_st + ckpt, sizeof s, cudaMemcpyDeviceToHost, c->stream), "state D2H");
         ck(cudaStreamSynchronize(c->stream), "ckpt read sync");
         if (step) *step = s.step;
@@ -687,8 +894,8 @@ int smx_ckpt_write(smx_ctx* c, int ckpt, const float* w, const float* m, int64_t
         check_ckpt(c, ckpt);
         cudaSetDevice(c->device);
         float* base = c->pool + c->slab_stride() * ckpt;
-        ck(cudaMemcpyAsync(base, w, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
-        ck(cudaMemcpyAsync(base + kPAlloc, m, sizeof(float) * kPAlloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
+        ck(cudaMemcpyAsync(base, w, sizeof(float) * c->palloc, cudaMemcpyHostToDevice, c->stream), "w H2D");
+        ck(cudaMemcpyAsync(base + c->palloc, m, sizeof(float) * c->palloc, cudaMemcpyHostToDevice, c->stream), "m H2D");
         SlotState s{step, offset};
         ck(cudaMemcpyAsync(c->ck_st + ckpt, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state H2D");
         ck(cudaStreamSynchronize(c->stream), "ckpt write sync");
@@ -730,7 +937,7 @@ int smx_train(smx_ctx* c, int n_active, const int* slots, int n_steps) {
             smx_ctx::Graph& g = graph_for(c, v);
             for (int i = 0; i < n_steps; ++i) {
                 ck(cudaGraphLaunch(g.exec, c->stream), "graph launch");
-                c->stats.launches += 14;
+                c->stats.launches += c->lockstep_launches;
             }
         } else {
             ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n_active, cudaMemcpyHostToDevice, c->stream),
@@ -753,6 +960,14 @@ int smx_eval(smx_ctx* c, int n, const int* slots, double* out) {
             for (int i = 0; i < k; ++i) check_slot(c, slots[base + i]);
             ck(cudaMemcpyAsync(c->eval_slots, slots + base, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream),
                "eval slots H2D");
+            if (c->cnn) {
+                eval_cnn(c, k);
+                ck(cudaMemcpyAsync(out + 2LL * base, c->eval_out, sizeof(double) * 2 * k, cudaMemcpyDeviceToHost,
+                                   c->stream),
+                   "eval D2H");
+                ck(cudaStreamSynchronize(c->stream), "eval sync");
+                continue;
+            }
             // Activations are addressed by position in the chunk, weights by slot id: each slot
             // runs its three forward GEMMs as a one-group launch (M = n_val fills the GPU).
             float* H1 = c->eval_act;
@@ -843,13 +1058,13 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             for (int i = 0; i < n; ++i) v[i] = i;
             ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
             StepCtx sc = step_ctx(c, c->scratch_slots);
-            const long long n4 = kPAlloc / 4;
+            const long long n4 = c->palloc / 4;
             const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
             for (int w = 0; w < 3; ++w)
-                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, kPAlloc, n4);
+                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, c->palloc, n4);
             cudaEventRecord(c->ev[6], c->stream);
             for (int r = 0; r < reps; ++r)
-                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, kPAlloc, n4);
+                sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, c->palloc, n4);
             cudaEventRecord(c->ev[7], c->stream);
         } else if (kind == 1) {
             if (n > c->C || n > c->S) fail(SMX_ECONFIG, "more checkpoints than allocated");
@@ -863,10 +1078,27 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
                 ck(cudaMalloc(&c->jobs, sizeof(CopyJob) * c->jobs_cap), "jobs");
             }
             ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
-            const long long n4 = 2 * kPAlloc / 4;
+            const long long n4 = 2 * c->palloc / 4;
             for (int w = 0; w < 3; ++w) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
             cudaEventRecord(c->ev[6], c->stream);
             for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
+            cudaEventRecord(c->ev[7], c->stream);
+        } else if ((kind == 2 || kind == 3) && c->cnn) {
+            if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
+            std::vector<int> v(n);
+            for (int i = 0; i < n; ++i) v[i] = i;
+            ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+            const cnn::ConvArgs a = cnn_args(c, c->scratch_slots);
+            c->cur = c->stream;
+            auto launch = [&] {
+                if (kind == 2)
+                    conv_forward<2>(c, a, n, c->d.max_batch);
+                else
+                    conv_wgrad<2>(c, a, n, c->d.max_batch);
+            };
+            for (int w = 0; w < 3; ++w) launch();
+            cudaEventRecord(c->ev[6], c->stream);
+            for (int r = 0; r < reps; ++r) launch();
             cudaEventRecord(c->ev[7], c->stream);
         } else if (kind == 2 || kind == 3) {
             // the two largest GEMMs of a lockstep at bs = 128 over n slots: 2 = fwd1 (X W1^T),

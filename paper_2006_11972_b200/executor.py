@@ -17,6 +17,7 @@ LIB_PATH = _PKG / "libsmx.so"
 
 SMX_OK, SMX_ECONFIG, SMX_EINTEGRITY, SMX_EDEVICE = 0, 1, 2, 3
 MODEL_MLP = 0
+MODEL_CNN = 1
 GEMM_EXACT, GEMM_TC = 0, 1
 HP_COLS = 4
 MET_COLS = 2

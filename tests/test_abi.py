@@ -26,7 +26,8 @@ def test_library_exports_every_declared_symbol():
 def test_constants_match_header():
     for name, val in [("SMX_OK", ex.SMX_OK), ("SMX_ECONFIG", ex.SMX_ECONFIG), ("SMX_EINTEGRITY", ex.SMX_EINTEGRITY),
                       ("SMX_EDEVICE", ex.SMX_EDEVICE), ("SMX_GEMM_EXACT", ex.GEMM_EXACT), ("SMX_GEMM_TC", ex.GEMM_TC),
-                      ("SMX_HP_COLS", ex.HP_COLS), ("SMX_MET_COLS", ex.MET_COLS), ("SMX_MODEL_MLP", ex.MODEL_MLP)]:
+                      ("SMX_HP_COLS", ex.HP_COLS), ("SMX_MET_COLS", ex.MET_COLS), ("SMX_MODEL_MLP", ex.MODEL_MLP),
+                      ("SMX_MODEL_CNN", ex.MODEL_CNN)]:
         m = re.search(rf"#define {name} (\d+)", HEADER)
         assert m and int(m.group(1)) == val, name
 

@@ -1,0 +1,158 @@
+"""CNN model on the GPU (SMX_MODEL_CNN) against the CPU oracle (oracle/cnn.c):
+
+* exact mode: dataset, init, multi-step trajectories (lr / momentum / wd / batch-size changes),
+  loss history and eval metrics are bit-identical to the oracle;
+* tensor-core mode (implicit-GEMM tcgen05 convolutions, 3xTF32): first-step loss and every
+  gradient within the stated tolerance, short trajectories within the fp32 envelope, results
+  grouping-invariant and run-to-run deterministic (bitwise);
+* the engine runs a merged CNN study whose metrics equal the oracle's (exact mode).
+"""
+import json
+
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+from paper_2006_11972_b200 import executor as ex
+from paper_2006_11972_b200 import host
+
+pytestmark = pytest.mark.gpu
+
+N_TRAIN, N_VAL, MAXB = 4096, 256, 64
+
+
+@pytest.fixture(scope="module")
+def ds():
+    return ol.cnn_dataset(N_TRAIN, N_VAL)
+
+
+def make(mode, slots=4, ckpts=2, max_steps=64):
+    return ex.Executor(n_slots=slots, n_ckpts=ckpts, gemm_mode=mode, max_steps=max_steps, max_batch=MAXB,
+                       n_train=N_TRAIN, n_val=N_VAL, model=ex.MODEL_CNN)
+
+
+def schedule(n, bs0=16, bs1=24):
+    hp = np.zeros((n, 4), np.float32)
+    for i in range(n):
+        hp[i] = [0.05 if i < n // 2 else 0.02, 0.9 if i % 3 else 0.5, 1e-4 if i < n // 3 else 1e-3,
+                 bs0 if i < n // 2 else bs1]
+    return hp
+
+
+def test_dataset_and_init_match_oracle(ds):
+    with make(ex.GEMM_EXACT) as e:
+        assert e.p_algo == 94538
+        assert e.dataset_digest() == ds.digest()
+        e.slot_init(1)
+        w, m = e.slot_read(1)
+        o = ol.CnnSlot(ds)
+        assert np.array_equal(w, o.w) and not m.any()
+
+
+def test_exact_trajectory_bitwise(ds):
+    n = 6
+    hp = schedule(n)
+    with make(ex.GEMM_EXACT) as e:
+        e.slot_init(0)
+        e.hp_upload(0, 0, hp)
+        e.train([0], n)
+        w, m = e.slot_read(0)
+        loss = e.losses(0, 0, n)
+        met = tuple(e.eval([0])[0])
+        step, off = e.slot_state(0)
+    o = ol.CnnSlot(ds, max_steps=n + 1)
+    o.train(hp, n)
+    assert step == n and off == o.offset.value
+    assert np.array_equal(loss, o.loss[:n])
+    assert np.array_equal(w, o.w) and np.array_equal(m, o.m)
+    assert met == o.eval()
+
+
+def test_exact_grouping_and_save_load(ds):
+    hp = schedule(4)
+    with make(ex.GEMM_EXACT) as e:
+        for s in range(3):
+            e.slot_init(s)
+            e.hp_upload(s, 0, hp if s != 1 else schedule(4, 32, 8))
+        e.train([0, 1, 2], 2)
+        e.slot_save(0, 0)
+        e.train([0, 1, 2], 2)
+        e.slot_load(2, 0)           # slot 2 restarts from slot 0's step-2 checkpoint
+        e.hp_upload(2, 0, hp)
+        e.train([2], 2)
+        w0, m0 = e.slot_read(0)
+        w2, m2 = e.slot_read(2)
+    assert np.array_equal(w0, w2) and np.array_equal(m0, m2)
+
+
+def rel(a, b):
+    return np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30)
+
+
+def test_tc_first_step_gradient(ds):
+    _, _, off = ol.cnn_layout()
+    for bs in (16, 64):
+        hp = np.tile(np.float32([1.0, 0.0, 0.0, bs]), (4, 1))   # m_1 = gradient
+        with make(ex.GEMM_TC) as e:
+            e.slot_init(0)
+            e.hp_upload(0, 0, hp)
+            e.train([0], 1)
+            _, m = e.slot_read(0)
+            loss = e.losses(0, 0, 1)[0]
+        o = ol.CnnSlot(ds, max_steps=4)
+        o.train(hp, 1)
+        assert abs(loss - o.loss[0]) <= 2e-6 * abs(o.loss[0])
+        for a, b in zip(off[:8], off[1:9]):
+            assert rel(m[a:b], o.m[a:b]) <= 2e-5, (bs, a, b, rel(m[a:b], o.m[a:b]))
+
+
+def test_tc_trajectory_and_eval_within_tolerance(ds):
+    n = 20
+    hp = schedule(n)
+    with make(ex.GEMM_TC) as e:
+        e.slot_init(0)
+        e.hp_upload(0, 0, hp)
+        e.train([0], n)
+        w, _ = e.slot_read(0)
+        loss = e.losses(0, 0, n)
+        vl, va = e.eval([0])[0]
+    o = ol.CnnSlot(ds, max_steps=n + 1)
+    o.train(hp, n)
+    assert np.max(np.abs(loss - o.loss[:n]) / np.abs(o.loss[:n])) <= 1e-4
+    assert rel(w, o.w) <= 1e-4
+    ovl, ova = o.eval()
+    assert abs(vl - ovl) <= 1e-4 * abs(ovl) and abs(va - ova) <= 2 / N_VAL
+
+
+def test_tc_grouping_invariance_and_determinism(ds):
+    hp = schedule(3)
+    outs = []
+    for group in ([0], [0, 1, 2, 3], [3, 0]):
+        with make(ex.GEMM_TC) as e:
+            for s in range(4):
+                e.slot_init(s)
+                e.hp_upload(s, 0, hp if s == 0 else schedule(3, 64, 40))
+            e.train(group, 3)
+            outs.append((*e.slot_read(0), e.losses(0, 0, 3), tuple(e.eval([0])[0])))
+    for o in outs[1:]:
+        assert all(np.array_equal(a, b) for a, b in zip(o[:3], outs[0][:3])) and o[3] == outs[0][3]
+
+
+def test_engine_cnn_study_exact_vs_oracle(ds):
+    spec = json.dumps({
+        "schema": 1, "name": "cnn_mini", "model": "cnn", "max_steps": 6,
+        "space": {"lr": [{"family": "step", "initial": "0.05", "gamma": "0.1", "milestones": [3]},
+                         {"family": "constant", "value": "0.05"}],
+                  "batch_size": [{"family": "constant", "value": 16}]},
+        "sampler": {"kind": "grid"}})
+    e = host.Engine.for_study(spec, slots_per_gpu=2, max_batch=MAXB, n_train=N_TRAIN, n_val=N_VAL, gemm_mode=0)
+    e.submit_study(spec)
+    e.run()
+    st = e.stats()
+    assert st["stage_steps"] == 9 and st["trial_steps"] == 12
+    info = host.expand_study(spec)
+    from test_engine_gpu import hp_table
+    for (study, trial), hist in e.histories().items():
+        o = ol.CnnSlot(ds, max_steps=8)
+        o.train(hp_table(info["trials"][trial]), 6)
+        assert [(s, l, a) for s, l, a in hist] == [(6, *o.eval())]
