@@ -32,6 +32,9 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
+# DRAM bytes (read + write) per launch of the roofline kernel from one `ncu --set full` capture
+# (profiles/<round>/), keyed by kernel; filled in after each capture.
+TRAFFIC: dict = {}
 METRIC = "trial-equivalent train steps/sec per study"
 UNIT = "trial-steps/s"
 
@@ -129,30 +132,36 @@ def reduce_sum(x: float, world: int) -> float:
 
 
 WORKLOADS = {
-    # name: (study spec, tuned?, description)
+    # name: (study spec, tuned?, description, slots per GPU, max batch)
+    "c2": ("c2_grid", False, "C2 grid (8 lr step-decays x 8 momentum sequences = 64 trials x 1200 steps, bs 128), "
+                             "CNN 3x32x32 conv 32/64/128 + GAP + FC, {n} replica stud{ies} (one per rank)", 64, 128),
     "c3": ("c3_random", False, "C3 space x {n} studies (256 random trials x 2000 steps each, seeds 0..{n1}), "
-                               "MLP 784-256-256-10, merged plan, root subtrees partitioned over ranks"),
+                               "MLP 784-256-256-10, merged plan, root subtrees partitioned over ranks", 128, 256),
     "c4_sha": ("c4_sha", True, "C4 SHA (eta 4, rungs 150/600/1200 steps, 448-trial grid), MLP 784-256-256-10, "
-                               "one study per rank (replicas)"),
+                               "one study per rank (replicas)", 128, 256),
     "c4_asha": ("c4_asha", True, "C4 ASHA (eta 4, rungs 150/600/1200 steps, 448-trial grid, 128 in flight), "
-                                 "MLP 784-256-256-10, one study per rank (replicas)"),
+                                 "MLP 784-256-256-10, one study per rank (replicas)", 128, 256),
 }
+DEFAULT_WORKLOAD = "c2"  # BASELINE.json configs[1]: the 1-GPU CNN grid search
 
 
 def workload(name: str, n_studies: int):
     """Study specs of a workload; sampler seeds 0..n-1 for the partitioned (untuned) ones."""
     from paper_2006_11972_b200 import host
 
-    spec_name, tuned, desc = WORKLOADS[name]
+    spec_name, tuned, desc = WORKLOADS[name][:3]
     base = json.loads(host.study_spec(spec_name))
+    desc = desc.format(n=n_studies, n1=n_studies - 1, ies="y" if n_studies == 1 else "ies")
     if tuned:
-        return [json.dumps(base)], True, desc.format(n=n_studies, n1=n_studies - 1)
+        return [json.dumps(base)], True, desc
+    if base.get("sampler", {}).get("kind") != "random":  # grid: identical replica per rank
+        return [json.dumps(base)], False, desc
     specs = []
     for s in range(n_studies):
         sp = dict(base)
         sp["sampler"] = {**base["sampler"], "seed": s}
         specs.append(json.dumps(sp))
-    return specs, False, desc.format(n=n_studies, n1=n_studies - 1)
+    return specs, False, desc
 
 
 def cuda_time(fn, world):
@@ -181,6 +190,7 @@ def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
     from paper_2006_11972_b200 import host
 
     info = host.expand_study(specs[0])
+    cnn = info["key"]["model"] == "cnn"
     cores = os.cpu_count() or 1
     n = max(cores, 8)
     hp = []
@@ -190,10 +200,11 @@ def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
         for c, name in enumerate(("lr", "momentum", "weight_decay", "batch_size")):
             rows[:, c] = r["hps"][name]["values"] if name in r["hps"] else [0.1, 0.9, 0.0, 128][c]
         hp.append(rows)
-    ds = ol.dataset()
+    ds = ol.cnn_dataset(65536, 4096, 128) if cnn else ol.dataset()
     T = min(int(info["max_steps"]), 2000)
-    slots = [ol.Slot(max_steps=T + 1) for _ in range(n)]
+    slots = [ol.CnnSlot(ds, max_steps=T + 1) for _ in range(n)] if cnn else [ol.Slot(max_steps=T + 1) for _ in range(n)]
     lib = ol.oracle()
+    train_many = lib.orc_cnn_train_many if cnn else lib.orc_train_many
     FP = ctypes.POINTER(ctypes.c_float)
     W = (FP * n)(*[ol.fp(s.w) for s in slots])
     M = (FP * n)(*[ol.fp(s.m) for s in slots])
@@ -202,9 +213,9 @@ def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
     step = (ctypes.c_int64 * n)()
     off = (ctypes.c_int64 * n)()
     done, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < seconds and done + 2 <= T:
-        k = 2
-        rc = lib.orc_train_many(n, W, M, step, off, H, T, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
+    k = 1 if cnn else 2
+    while time.perf_counter() - t0 < seconds and done + k <= T:
+        rc = train_many(n, W, M, step, off, H, T, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
         assert rc == 0
         done += k
     dt = time.perf_counter() - t0
@@ -219,7 +230,7 @@ def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (oracle port of the executor on the same plan)."""
     if rank != 0:
         return
-    specs, _, _ = workload("c3", 1)
+    specs, _, desc = workload(args.workload, 1)
     from paper_2006_11972_b200 import host
 
     info = host.expand_study(specs[0])
@@ -233,8 +244,7 @@ def run_reference(args, rank, world):
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                       "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
                       "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                      "config": {"workload": "C3 space x 1 study (256 random trials x 2000 steps), MLP 784-256-256-10",
-                                 "flush": "n/a (CPU)"},
+                      "config": {"workload": desc, "flush": "n/a (CPU)"},
                       "cpu_baseline": {**cb, "value": v},
                       "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
           flush=True)
@@ -247,11 +257,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--gemm", default=os.environ.get("SMX_BENCH_GEMM", "tc"), choices=["exact", "tc"])
-    ap.add_argument("--slots", type=int, default=128)
+    ap.add_argument("--slots", type=int, default=0, help="slots per GPU (0: the workload's default)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-trial", action="store_true", help="skip the TRIAL-mode (unmerged) comparison run")
     args = ap.parse_args()
+    if not args.slots:
+        args.slots = WORKLOADS[args.workload][3]
     rank, world, local = dist_init()
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -265,9 +277,13 @@ def main():
     specs, tuned, desc = workload(args.workload, world)
     info = host.expand_study(specs[0])
     gemm_mode = ex.GEMM_TC if args.gemm == "tc" else ex.GEMM_EXACT
-    part = {} if tuned else {"rank": rank, "world": world}  # tuned studies: one replica per rank
+    # random-sampled studies differ per rank and are merged + root-partitioned; tuned studies and
+    # grids run one replica per rank
+    part = {"rank": rank, "world": world} if (not tuned and len(specs) == world and world > 1) else {}
+    cnn = info["key"]["model"] == "cnn"
+    max_batch = WORKLOADS[args.workload][4]
     eng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
-                                gemm_mode=gemm_mode, max_steps=2048, **part)
+                                gemm_mode=gemm_mode, max_steps=2048, max_batch=max_batch, **part)
 
     def submit_and_run(e):
         if tuned:
@@ -296,7 +312,8 @@ def main():
 
     import oracle_lib as ol
 
-    ds = ol.dataset()  # host copy of the dataset (bit-identical to the on-device generator)
+    # host copy of the dataset (bit-identical to the on-device generator)
+    ds = ol.cnn_dataset(65536, 4096, max_batch) if cnn else ol.dataset()
     lib = ex.load_library()
     pinned = []
     host_arrays = []
@@ -326,7 +343,8 @@ def main():
     savings = None
     if not args.no_trial:
         teng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
-                                     gemm_mode=gemm_mode, max_steps=2048, trial_mode=True, **part)
+                                     gemm_mode=gemm_mode, max_steps=2048, max_batch=max_batch, trial_mode=True,
+                                     **part)
 
         def one_trial():
             teng.reset()
@@ -347,17 +365,21 @@ def main():
     # 64-slot context of the same GPU (bs 128, the study's typical active set)
     pk = peaks()
     n_k = 64
-    kx = ex.Executor(n_slots=n_k, n_ckpts=16, device=local, max_steps=64, gemm_mode=gemm_mode)
+    kx = ex.Executor(n_slots=n_k, n_ckpts=16, device=local, max_steps=64, gemm_mode=gemm_mode, max_batch=max_batch,
+                     model=ex.MODEL_CNN if cnn else ex.MODEL_MLP)
     for s_ in range(n_k):
         kx.slot_init(s_)
         kx.hp_upload(s_, 0, np.tile(np.float32([0.05, 0.9, 1e-4, 128]), (64, 1)))
     kx.train(list(range(n_k)), 1)  # produce activations / gradients once
     kx.sync()
     ms = {kind: kx.bench_kernel(kind, n_k if kind != 1 else 16, 30) for kind in (0, 1, 2, 3)}
+    P = kx.p_algo
     kx.close()
-    P = 269322
     upd_bytes, fork_bytes = 20 * P * n_k, 16 * P * 16
-    gemm_flops = 2 * 128 * 256 * 784 * n_k  # per launch, both layer-1 GEMMs at bs 128
+    if cnn:  # conv2: M = 128 x 16 x 16 output pixels, N = 64, K = 9 x 32 (both kinds)
+        gemm_flops = 2 * 128 * 256 * 288 * 64 * n_k
+    else:  # layer 1: 128 x 256 x 784 (both kinds)
+        gemm_flops = 2 * 128 * 256 * 784 * n_k
     tc_peak = pk["bf16_tflops"]
 
     def hbm(name, b, t, **kw):
@@ -372,15 +394,26 @@ def main():
                 "note": "fp32-equivalent flops; 3xTF32 issues 3 kind::tf32 MMAs (tf32 = bf16/2) per product, so "
                         "the mode's own ceiling is bf16/6 = %.0f TFLOP/s" % (tc_peak / 6)}
 
-    kernels = {
-        "K1_fwd1_gemm": tensor("fwd1", gemm_flops, ms[2]),
-        "K3_wgrad1_gemm": tensor("wgrad1", gemm_flops, ms[3]),
-        "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_k),
-        "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=16),
-    }
-    roofline = dict(kernels["K1_fwd1_gemm"])
-    roofline["traffic"] = None
-    roofline["kernel"] = "gemm_tc_kernel<0,0,BiasRelu> (layer-1 forward, 64 groups x 128x256x784)"
+    if cnn:
+        kernels = {
+            "K1_conv2_fwd": tensor("fwd", gemm_flops, ms[2]),
+            "K3_conv2_wgrad": tensor("wgrad", gemm_flops, ms[3]),
+            "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_k),
+            "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=16),
+        }
+        roofline = dict(kernels["K1_conv2_fwd"])
+        roofline["kernel"] = ("conv_tc_kernel<Fwd<2>> (conv2 implicit GEMM, 64 groups x M 32768 x N 64 x K 288)"
+                              if gemm_mode == ex.GEMM_TC else "conv_fwd_simt<2>")
+    else:
+        kernels = {
+            "K1_fwd1_gemm": tensor("fwd1", gemm_flops, ms[2]),
+            "K3_wgrad1_gemm": tensor("wgrad1", gemm_flops, ms[3]),
+            "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_k),
+            "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=16),
+        }
+        roofline = dict(kernels["K1_fwd1_gemm"])
+        roofline["kernel"] = "gemm_tc_ts_kernel<0,0,BiasRelu> (layer-1 forward, 64 groups x 128x256x784)"
+    roofline["traffic"] = TRAFFIC.get(roofline["kernel"].split(" ")[0])
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -395,7 +428,8 @@ def main():
                        "gemm": args.gemm, "slots_per_gpu": args.slots, "trials": len(info["trials"]) * len(specs),
                        "trial_steps": trial_steps, "unique_stage_steps": stage_steps,
                        "executed_merge_rate": trial_steps / stage_steps,
-                       "flush": "inputs > L2: per-slot state 2.2 MB x 128 slots + 206 MB dataset"},
+                       "flush": ("inputs > L2: per-slot activations 60 MB x 64 slots + 1.07 GB dataset" if cnn else
+                                 "inputs > L2: per-slot state 2.2 MB x 128 slots + 206 MB dataset")},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": st_e["h2d_bytes"], "d2h_bytes_per_step": st_e["d2h_bytes"]},
             "gpu_launches": st["kernel_launches"] * args.steps,

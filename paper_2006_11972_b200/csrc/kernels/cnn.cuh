@@ -411,6 +411,15 @@ using namespace smx::tc3;
 
 enum { kEpiBiasRelu = 0, kEpiMask = 1, kEpiPartT = 2 };
 constexpr int kConvSmem = kSmem + 512;  // + the tile's bias slice
+// TMEM: two accumulator regions (columns [0,128) and [128,256)) used for alternating segments
+// of kSeg chunks, then the A operand hi/lo double buffer at 256 + 64 b.  Each finished segment is
+// added into fp32 registers with round-to-nearest adds: the tensor core's own fp32 accumulation
+// is not round-to-nearest, and over long reductions (the weight gradients sum up to 2048 rows
+// per split) its error grows linearly; promoting every kSeg * 32 = 64 products keeps the result
+// at fp32 accuracy.
+constexpr int kSeg = 2;
+constexpr int kConvTmemCols = 512;
+constexpr int kAOff = 256;
 
 // source of zero-filled 16-byte copies (cp.async reads 0 bytes from it)
 __device__ __align__(16) float kZero16[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols));
+                     "r"(kConvTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (threadIdx.x == 0) {
@@ -627,6 +636,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
     if (total > 1) issue(1);
     asm volatile("cp.async.commit_group;");
     float a_cur[kAK];
+    const int cols = nt / kParts;  // accumulator columns owned by this thread: [kpart*cols, +cols)
+    float racc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) racc[j] = 0.0f;
+    // add accumulator region `reg` into racc (round-to-nearest fp32 adds)
+    auto drain = [&](int reg) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            if (j < cols) {
+                uint32_t r[4];
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(reg * 128 + kpart * cols + j);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                             : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+                for (int q = 0; q < 4; ++q) racc[j + q] = __fadd_rn(racc[j + q], __uint_as_float(r[q]));
+            }
+        }
+    };
 
 #pragma unroll 1
     for (int g = 0; g < total; ++g) {
@@ -649,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
                 hi[i] = Op::A_EXACT ? a_cur[i] : tf32_rna(a_cur[i]);
                 lo[i] = tf32_rna(__fsub_rn(a_cur[i], hi[i]));
             }
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + 128 + b * 64 + kpart * kAK;
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + kAOff + b * 64 + kpart * kAK;
             tmem_st8(ta, hi);
             if (!Op::A_EXACT) tmem_st8(ta + 32, lo);
             asm volatile("tcgen05.wait::st.sync.aligned;");
@@ -666,43 +695,50 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
         if (threadIdx.x == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t bhi = hl_u32 + b * 2 * kTile, blo = bhi + kTile;
-            const uint32_t ahi = tmem + 128 + b * 64, alo = ahi + 32;
+            const uint32_t ahi = tmem + kAOff + b * 64, alo = ahi + 32;
+            const uint32_t dacc = tmem + (uint32_t)(((c / kSeg) & 1) * 128);
             const int ksteps = (min(kKC, klim - k0) + 7) / 8;
 #pragma unroll 1
             for (int s = 0; s < ksteps; ++s) {
                 const uint32_t o = s * 2 * kLbo;
                 const uint64_t dbh = smem_desc(bhi + o, kLbo, 128), dbl = smem_desc(blo + o, kLbo, 128);
-                uint32_t acc = (c == 0 && s == 0) ? 0u : 1u;
+                uint32_t acc = (c % kSeg == 0 && s == 0) ? 0u : 1u;
                 if (!Op::A_EXACT) {
-                    mma_ts(tmem, alo + s * 8, dbh, idesc, acc);
+                    mma_ts(dacc, alo + s * 8, dbh, idesc, acc);
                     acc = 1u;
                 }
                 if (!Op::B_EXACT) {
-                    mma_ts(tmem, ahi + s * 8, dbl, idesc, acc);
+                    mma_ts(dacc, ahi + s * 8, dbl, idesc, acc);
                     acc = 1u;
                 }
-                mma_ts(tmem, ahi + s * 8, dbh, idesc, acc);
+                mma_ts(dacc, ahi + s * 8, dbh, idesc, acc);
             }
             mma_commit(&bars[b]);
         }
-        if (c != nchunks - 1) continue;
+        if (c > 0 && c % kSeg == 0) {
+            // the previous segment (other accumulator region) is complete once chunk g-1's MMAs are
+            mbar_wait(&bars[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            drain(((c - 1) / kSeg) & 1);
+        }
+        if (c != nchunks - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            continue;
+        }
 
         // ---- epilogue of this tile (the next tile's loads are already in flight)
         mbar_wait(&bars[b], (g >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        drain((c / kSeg) & 1);
+        asm volatile("tcgen05.fence::before_thread_sync;");
         const int m = m0 + quad * 32 + lane;
-        const int cols = nt / kParts;
-        for (int c0 = kpart * cols; c0 < (kpart + 1) * cols; c0 += 4) {
-            uint32_t r[4];
-            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                         : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-            if (m >= M || c0 >= N) continue;
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+            const int c0 = kpart * cols + jj;
+            if (jj >= cols || m >= M || c0 >= N) continue;
             float x[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 4; ++j) x[j] = racc[jj + j];
             if constexpr (Op::EPI == kEpiBiasRelu) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -721,11 +757,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
                 for (int j = 0; j < 4; ++j) pt[(long long)(c0 + j) * Op::kPartLd] = x[j];
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) racc[j] = 0.0f;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kConvTmemCols));
 }
 
 }  // namespace ctc

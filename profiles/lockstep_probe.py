@@ -1,5 +1,5 @@
 """Profiling probe: a fixed number of grouped training locksteps on a typical active set
-(64 slots, bs 128, MLP) so ncu can capture every kernel of a lockstep.
+(64 slots, bs 128, MLP or CNN) so ncu can capture every kernel of a lockstep.
 
     python profiles/lockstep_probe.py [--gemm tc|exact] [--slots 64] [--steps 3] [--warmup 2]
 """
@@ -18,8 +18,10 @@ ap.add_argument("--slots", type=int, default=64)
 ap.add_argument("--bs", type=int, default=128)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--model", default="mlp", choices=["mlp", "cnn"])
 a = ap.parse_args()
-e = ex.Executor(n_slots=a.slots, n_ckpts=4, max_steps=64, gemm_mode=ex.GEMM_TC if a.gemm == "tc" else ex.GEMM_EXACT)
+e = ex.Executor(n_slots=a.slots, n_ckpts=4, max_steps=64, gemm_mode=ex.GEMM_TC if a.gemm == "tc" else ex.GEMM_EXACT,
+                model=ex.MODEL_CNN if a.model == "cnn" else ex.MODEL_MLP)
 e.set_graphs(False)
 hp = np.tile(np.float32([0.05, 0.9, 1e-4, a.bs]), (64, 1))
 for s in range(a.slots):

@@ -162,8 +162,8 @@ class CnnDataset:
 
 
 @lru_cache(None)
-def cnn_dataset(n_train=N_TRAIN, n_val=N_VAL) -> CnnDataset:
-    return CnnDataset(n_train=n_train, n_val=n_val)
+def cnn_dataset(n_train=N_TRAIN, n_val=N_VAL, max_batch=MAX_BATCH) -> CnnDataset:
+    return CnnDataset(n_train=n_train, n_val=n_val, max_batch=max_batch)
 
 
 class CnnSlot:
