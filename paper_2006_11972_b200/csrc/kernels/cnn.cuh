@@ -55,9 +55,29 @@ struct Part {
     static constexpr long long Size = (long long)MaxSplit * Geo<L>::Co * Ld;
 };
 
+// layer-1 weight-gradient outputs: 32 co x 27 (tap, ci) + 32 bias
+constexpr int kL1Outs = 32 * 28;
+
 // Per-slot activation scratch: offsets in floats, tensors [max_batch][...] (computed on host).
 struct ActLayout {
-    long long a1, a2, a3, d1, d2, d3, g, z, dz, dg, rl, p1, p2, p3, stride;
+    long long a1, a2, a3, d1, d2, d3, g, z, dz, dg, rl, p1, p2, p3, wf1, wf2, wf3, wd2, wd3, w1p, stride;
+};
+
+// Tensor-core B operands that are weights are pre-split once per lockstep into "images": per K
+// chunk of 32, the tf32 hi tile then the lo tile, each in the UMMA K-major canonical layout
+// ((row r, k) at (k/4)*16*nt + (r/8)*128 + (r%8)*16 + (k%4)*4 bytes), so a stage is one bulk
+// async copy of nt*256 bytes.  Forward: rows co, K = (tap, ci); input gradient: rows ci, K per
+// parity class = (dense tap, co), classes back to back.
+template <int L>
+struct WImg {
+    static constexpr int FwdChunks = (9 * Geo<L>::Ci + 31) / 32;
+    static constexpr int FwdFloats = FwdChunks * Geo<L>::Co * 64;
+    static constexpr int DgrChunks = 9 * Geo<L>::Co / 32;
+    static constexpr int DgrFloats = DgrChunks * Geo<L>::Ci * 64;
+    // first chunk of parity class c (taps 1, 2, 2, 4)
+    static __host__ __device__ constexpr int class_chunk0(int c) {
+        return (c == 0 ? 0 : c == 1 ? 1 : c == 2 ? 3 : 5) * Geo<L>::Co / 32;
+    }
 };
 inline ActLayout act_layout(int max_batch) {
     ActLayout L{};
@@ -78,12 +98,23 @@ inline ActLayout act_layout(int max_batch) {
     L.dz = take(kNCP);
     L.dg = take(kFeat);
     L.rl = take(1);
+    L.w1p = take(kL1Outs);
     L.p1 = o;
     o += Part<1>::Size;
     L.p2 = o;
     o += Part<2>::Size;
     L.p3 = o;
     o += Part<3>::Size;
+    L.wf1 = o;
+    o += WImg<1>::FwdFloats;
+    L.wf2 = o;
+    o += WImg<2>::FwdFloats;
+    L.wf3 = o;
+    o += WImg<3>::FwdFloats;
+    L.wd2 = o;
+    o += WImg<2>::DgrFloats;
+    L.wd3 = o;
+    o += WImg<3>::DgrFloats;
     L.stride = (o + 63) / 64 * 64;
     return L;
 }
@@ -429,14 +460,19 @@ template <int L>
 struct Fwd {
     using G = Geo<L>;
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu;
-    static constexpr bool A_EXACT = (L == 1), B_EXACT = false;
-    static constexpr int kOnesRow = -1, kPartLd = 0;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
     const float* in;
     const float* w;
     const float* bias;
     float* out;
+    const float* img;
     int M, N, K, kbeg, m0, split;
+    struct RowInfo {
+        int base, ih0, iw0;  // sample offset, top-left input pixel of the 3x3 window (-1: invalid row)
+    };
     __device__ void setup(const ConvArgs& p, const SlotView& v, int tile_y) {
+        img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
         in = layer_in<L>(p, v);
         w = v.w + G::OffW;
         bias = v.w + G::OffB;
@@ -455,6 +491,18 @@ struct Fwd {
         if (ih < 0 || ih >= G::H || iw < 0 || iw >= G::H) return nullptr;
         return in + (((long long)n * G::H + ih) * G::H + iw) * G::Ci + ci;
     }
+    __device__ __forceinline__ RowInfo row_info(int m) const {
+        if (m >= M) return RowInfo{0, -1000, -1000};
+        const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
+        return RowInfo{n * G::H * G::H * G::Ci, (pix / G::OH) * G::S - 1, (pix % G::OH) * G::S - 1};
+    }
+    __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& r, int k) const {
+        const int t = k / G::Ci, ci = k % G::Ci;
+        const int ih = r.ih0 + t / 3, iw = r.iw0 + t % 3;
+        if ((unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H || k >= K) return nullptr;
+        return in + r.base + (ih * G::H + iw) * G::Ci + ci;
+    }
+    __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
     __device__ __forceinline__ float* c_row(int m) const { return out + (long long)m * G::Co; }
     __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
@@ -467,16 +515,21 @@ struct Dgrad {
     using G = Geo<L>;
     static_assert(G::S == 2, "parity decomposition is for stride 2");
     static constexpr int AM = 0, BMODE = 1, EPI = kEpiMask;
-    static constexpr bool A_EXACT = false, B_EXACT = false;
-    static constexpr int kOnesRow = -1, kPartLd = 0;
+    static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
     static constexpr int HH = G::H / 2;
     const float* dy;
     const float* w;
     const float* act;
     float* dx;
+    const float* img;
     int M, N, K, kbeg, m0, split;
     int pi, pj, nkw;  // class, taps per row of the class
+    struct RowInfo {
+        int base, ih, iw;  // sample offset in dy, input pixel (-1000: invalid row)
+    };
     __device__ void setup(const ConvArgs& p, const SlotView& v, int cls) {
+        img = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)WImg<L>::class_chunk0(cls) * G::Ci * 64;
         dy = layer_dout<L>(p, v);
         w = v.w + G::OffW;
         act = layer_out<L - 1>(p, v);
@@ -496,6 +549,20 @@ struct Dgrad {
         kh = pi ? 2 * jh : 1;
         kw = pj ? 2 * jw : 1;
     }
+    __device__ __forceinline__ RowInfo row_info(int r) const {
+        if (r >= M) return RowInfo{0, -1000, -1000};
+        const int n = r / (HH * HH), q = r % (HH * HH);
+        return RowInfo{n * G::OH * G::OH * G::Co, 2 * (q / HH) + pi, 2 * (q % HH) + pj};
+    }
+    __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& ri, int k) const {
+        int kh, kw;
+        tap(k / G::Co, kh, kw);
+        const int nh = ri.ih + 1 - kh, nw = ri.iw + 1 - kw;  // even by the class parity
+        const int oh = nh >> 1, ow = nw >> 1;
+        if (nh < 0 || nw < 0 || oh >= G::OH || ow >= G::OH || k >= K) return nullptr;
+        return dy + ri.base + (oh * G::OH + ow) * G::Co + k % G::Co;
+    }
+    __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     __device__ __forceinline__ long long pix_off(int r) const {
         const int n = r / (HH * HH), q = r % (HH * HH);
         const int ih = 2 * (q / HH) + pi, iw = 2 * (q % HH) + pj;
@@ -526,8 +593,25 @@ template <int L>
 struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT;
-    static constexpr bool A_EXACT = (L == 1), B_EXACT = false;
-    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false;
+    struct RowInfo {
+        int kh, kw, ci;  // tap and first channel of a row quad (kh = -1000: padding rows)
+    };
+    // rows row..row+3 = (tap, 4 consecutive channels)
+    __device__ __forceinline__ RowInfo row_info(int row) const {
+        if (row >= kOnesRow) return RowInfo{-1000, 0, 0};
+        const int t = row / G::Ci;
+        return RowInfo{t / 3 - 1, t % 3 - 1, row % G::Ci};
+    }
+    // the 4 rows of `ri` at reduction index m (sample, output pixel)
+    __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& ri, int m) const {
+        const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
+        const int ih = (pix / G::OH) * G::S + ri.kh, iw = (pix % G::OH) * G::S + ri.kw;
+        if ((unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H || m >= kbeg + K) return nullptr;
+        return in + ((n * G::H + ih) * G::H + iw) * G::Ci + ri.ci;
+    }
+    __device__ __forceinline__ const float* b_image(int) const { return nullptr; }
+    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld, kSegChunks = 4;
     const float* in;
     const float* dy;
     float* part;
@@ -766,6 +850,176 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int ti
 }
 
 }  // namespace ctc
+
+// Weight images (see WImg): one thread per 16-byte unit of the hi tile (and its lo twin).
+// grid (blocks, groups), block 256.
+__device__ __forceinline__ float tf32_rna_h(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+template <int L>
+__global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
+    using G = Geo<L>;
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const float* W = v.w + G::OffW;
+    const int fwd_units = WImg<L>::FwdChunks * 8 * G::Co;
+    const int dgr_units = (L >= 2) ? WImg<L>::DgrChunks * 8 * G::Ci : 0;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < fwd_units + dgr_units; u += gridDim.x * blockDim.x) {
+        float val[4];
+        float* dst;
+        int nt;
+        if (u < fwd_units) {  // rows co, k = (tap, ci)
+            nt = G::Co;
+            const int c = u / (8 * nt), kq = (u / nt) % 8, r = u % nt;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = c * 32 + kq * 4 + e;
+                val[e] = k < 9 * G::Ci ? W[r * 9 * G::Ci + k] : 0.0f;
+            }
+            dst = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3) + (long long)c * nt * 64 +
+                  (kq * nt * 16 + (r >> 3) * 128 + (r & 7) * 16) / 4;
+        } else {  // rows ci, per class k = (dense tap j, co)
+            const int uu = u - fwd_units;
+            nt = G::Ci;
+            const int cg = uu / (8 * nt), kq = (uu / nt) % 8, r = uu % nt;
+            int cls = 0;
+            while (cls < 3 && cg >= WImg<L>::class_chunk0(cls + 1)) ++cls;
+            const int c = cg - WImg<L>::class_chunk0(cls);
+            const int pi = cls >> 1, pj = cls & 1, nkw = pj ? 2 : 1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = c * 32 + kq * 4 + e;
+                const int j = k / G::Co, co = k % G::Co;
+                const int kh = pi ? 2 * (j / nkw) : 1, kw = pj ? 2 * (j % nkw) : 1;
+                val[e] = W[(co * 9 + kh * 3 + kw) * G::Ci + r];
+            }
+            dst = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)cg * nt * 64 +
+                  (kq * nt * 16 + (r >> 3) * 128 + (r & 7) * 16) / 4;
+        }
+        float4 hi, lo;
+        hi.x = tf32_rna_h(val[0]); lo.x = tf32_rna_h(__fsub_rn(val[0], hi.x));
+        hi.y = tf32_rna_h(val[1]); lo.y = tf32_rna_h(__fsub_rn(val[1], hi.y));
+        hi.z = tf32_rna_h(val[2]); lo.z = tf32_rna_h(__fsub_rn(val[2], hi.z));
+        hi.w = tf32_rna_h(val[3]); lo.w = tf32_rna_h(__fsub_rn(val[3], hi.w));
+        *reinterpret_cast<float4*>(dst) = hi;
+        *reinterpret_cast<float4*>(dst + nt * 32) = lo;  // lo tile follows the hi tile (nt*128 bytes)
+    }
+}
+
+// ---- layer 1 in tensor-core mode: fp32 SIMT kernels ---------------------------------------
+// conv1 has K = 27 and N = 32: far too thin for 128-row tcgen05 tiles, and memory-bound anyway.
+// These kernels use plain fp32 FMA (at least as accurate as 3xTF32) in their own fixed order;
+// exact mode keeps the oracle-order kernels above.
+
+// One thread per output pixel, all 32 channels in registers; W1^T staged in shared memory and
+// read as warp-uniform broadcasts.  grid (ceil(max_batch*1024/256), groups), block 256.
+__global__ void __launch_bounds__(256) conv1_fwd_fast(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    __shared__ __align__(16) float wt[27][32];
+    __shared__ float bs_[32];
+    for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
+        const int co = i & 31, k = i >> 5, t = k / 3, ci = k % 3;
+        wt[k][co] = v.w[Geo<1>::OffW + (co * 9 + t) * 4 + ci];
+    }
+    if (threadIdx.x < 32) bs_[threadIdx.x] = v.w[Geo<1>::OffB + threadIdx.x];
+    __syncthreads();
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= v.bs * 1024) return;
+    const float* in = layer_in<1>(p, v);
+    const int n = m >> 10, oh = (m >> 5) & 31, ow = m & 31;
+    float acc[32];
+#pragma unroll
+    for (int co = 0; co < 32; ++co) acc[co] = bs_[co];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int ih = oh + t / 3 - 1, iw = ow + t % 3 - 1;
+        if ((unsigned)ih >= 32u || (unsigned)iw >= 32u) continue;
+        const float4 x = __ldg(reinterpret_cast<const float4*>(in + (((n << 5) + ih) * 32 + iw) * 4));
+        const float xv[3] = {x.x, x.y, x.z};
+#pragma unroll
+        for (int ci = 0; ci < 3; ++ci) {
+            const float4* wr = reinterpret_cast<const float4*>(wt[t * 3 + ci]);
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+                const float4 w4 = wr[c4];
+                acc[4 * c4] = __fmaf_rn(xv[ci], w4.x, acc[4 * c4]);
+                acc[4 * c4 + 1] = __fmaf_rn(xv[ci], w4.y, acc[4 * c4 + 1]);
+                acc[4 * c4 + 2] = __fmaf_rn(xv[ci], w4.z, acc[4 * c4 + 2]);
+                acc[4 * c4 + 3] = __fmaf_rn(xv[ci], w4.w, acc[4 * c4 + 3]);
+            }
+        }
+    }
+    float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)m * 32);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4)
+        out[c4] = make_float4(fmaxf(acc[4 * c4], 0.0f), fmaxf(acc[4 * c4 + 1], 0.0f), fmaxf(acc[4 * c4 + 2], 0.0f),
+                              fmaxf(acc[4 * c4 + 3], 0.0f));
+}
+
+// Per-sample partial weight gradient of conv1: block = one (sample, slot); lane = output channel,
+// 28 accumulators per lane (27 taps x channels + bias); the sample's zero-padded image is staged
+// in shared memory and read as warp-uniform broadcasts; the 8 warps' partials are combined in a
+// fixed order.  partial[n][co*28 + j].  grid (max_batch, groups), block 256.
+__global__ void __launch_bounds__(256) conv1_wgrad_fast(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    const int n = blockIdx.x;
+    if (n >= v.bs) return;
+    __shared__ __align__(16) float img[34 * 34 * 4];
+    __shared__ float red[8][kL1Outs];
+    const float* in = layer_in<1>(p, v) + (long long)n * 4096;
+    for (int i = threadIdx.x; i < 34 * 34; i += blockDim.x) {
+        const int y = i / 34 - 1, x = i % 34 - 1;
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((unsigned)y < 32u && (unsigned)x < 32u) val = __ldg(reinterpret_cast<const float4*>(in + (y * 32 + x) * 4));
+        reinterpret_cast<float4*>(img)[i] = val;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, co = threadIdx.x & 31;
+    const float* dy = layer_dout<1>(p, v) + (long long)n * 1024 * 32;
+    float acc[28];
+#pragma unroll
+    for (int j = 0; j < 28; ++j) acc[j] = 0.0f;
+    for (int pix = warp * 128; pix < warp * 128 + 128; ++pix) {
+        const float d = dy[pix * 32 + co];
+        const int oh = pix >> 5, ow = pix & 31;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+            const float4 x = reinterpret_cast<const float4*>(img)[(oh + t / 3) * 34 + ow + t % 3];
+            acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
+            acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
+            acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
+        }
+        acc[27] = __fadd_rn(acc[27], d);
+    }
+#pragma unroll
+    for (int j = 0; j < 28; ++j) red[warp][co * 28 + j] = acc[j];
+    __syncthreads();
+    float* part = v.act + p.al.w1p + (long long)n * kL1Outs;
+    for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
+        float s_ = red[0][i];
+        for (int w = 1; w < 8; ++w) s_ = __fadd_rn(s_, red[w][i]);
+        part[i] = s_;
+    }
+}
+
+// Sum the per-sample partials in sample order into the gradient slab.  grid (groups), block 256.
+__global__ void __launch_bounds__(256) conv1_wgrad_reduce(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.x]);
+    const float* part = v.act + p.al.w1p;
+    float* g = p.grad + p.grad_stride * v.slot;
+    for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
+        float s_ = 0.0f;
+        for (int n = 0; n < v.bs; ++n) s_ = __fadd_rn(s_, part[(long long)n * kL1Outs + i]);
+        const int co = i / 28, j = i % 28;
+        if (j < 27)
+            g[Geo<1>::OffW + (co * 9 + j / 3) * 4 + j % 3] = s_;
+        else
+            g[Geo<1>::OffB + co] = s_;
+    }
+    // the padded input channel's weights stay exactly zero
+    for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) g[Geo<1>::OffW + i * 4 + 3] = 0.0f;
+}
 
 // Weight-gradient reduction: grad[W][co][k] = sum_{s asc} part[s][co][k] (k < 9 Ci), grad[b][co]
 // from the all-ones row.  grid (Co, groups), block 128.

@@ -1,0 +1,462 @@
+// Warp-specialised implicit-GEMM convolution on tcgen05 (3xTF32), the tensor-core path of the
+// CNN (replaces the lock-step conv_tc_kernel structure: no CTA-wide barrier per K chunk).
+//
+//   warps 0-7   producers: gather the A tile (128 rows x 32 k) and the B tile (N x 32 k) of a K
+//               chunk from global memory through the Op's implicit-GEMM address functions,
+//               split each value into tf32 hi/lo, write A hi/lo to TMEM (tcgen05.st, lane = row)
+//               and B hi/lo to shared memory in the UMMA K-major canonical layout, then arrive
+//               on the stage's `full` mbarrier.  3-stage ring; K-contiguous A tiles are
+//               staged by coalesced cp.async (3 deep) and read back row-wise.
+//   warp 12     MMA issuer (one elected thread): per chunk 3 (2 when an operand is exact in tf32)
+//               tcgen05.mma kind::tf32 per 8-k step into the tile's TMEM accumulator, commit
+//               -> the stage's `empty` barrier; after a tile's last chunk commit -> `acc_full`.
+//   warps 8-11  epilogue: tcgen05.ld the accumulator (lane quadrant = warp % 4), release it
+//               (`acc_empty`), apply bias+ReLU / ReLU-mask / transposed partial store.
+// Two TMEM accumulators alternate between consecutive accumulation units — M tiles, or for the
+// weight gradients (Op::kSegChunks > 0) segments of kSegChunks chunks of one tile — so draining
+// one unit overlaps the MMAs of the next.  Segmented units are added into an fp32 tile in shared
+// memory with round-to-nearest adds: the tensor core's fp32 accumulation is not
+// round-to-nearest, and over the 2048-row weight-gradient reductions its error grows to ~4e-5;
+// promoting every 64 products keeps the result at fp32 accuracy.
+// TMEM columns: acc0 [0,128), acc1 [128,256), A stages [256 + 64 s, +64) (hi at +0, lo at +32).
+// Shared memory: 3 B stages (hi, lo; 32 KB) | 3 raw A tiles (18 KB) | barriers | segment sums (64 KB).
+// Results depend only on the group's own operands and the fixed tile/chunk order: deterministic
+// and grouping-invariant like every executor kernel.
+#pragma once
+
+#include "cnn.cuh"
+
+namespace smx {
+namespace cnn {
+namespace ws {
+
+using namespace smx::tc3;
+
+constexpr int kStages = 3;                       // B smem / A TMEM ring
+constexpr int kARaw = 3;                         // producer-side cp.async ring of raw A tiles
+constexpr int kProducers = 256;                  // warps 0-7
+constexpr int kEpiWarp0 = 8;                     // warps 8-11
+constexpr int kMmaWarp = 12;
+constexpr int kWsThreads = 13 * 32;
+constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K-major canonical, N <= 128
+constexpr int kBStage = 2 * kBTile;
+constexpr int kARawTile = kBM * kRawLdK * 4;     // raw A tile [128 rows][32 + 4 pad]
+constexpr int kBarOff = kStages * kBStage + kARaw * kARawTile;
+constexpr int kWsSmem = kBarOff + 128;
+constexpr int kSaccBytes = kBM * 128 * 4;        // segment-sum tile, float4 [col/4][row][4]
+template <class Op>
+constexpr int ws_smem() {
+    return kWsSmem + (Op::kSegChunks > 0 ? kSaccBytes : 0);
+}
+constexpr int kWsTmemCols = 512;
+constexpr int kAcc = 128;                        // columns per accumulator
+constexpr int kABase = 256;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+    return p ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void split1(float a, float& h, float& l) {
+    h = EXACT ? a : tf32_rna(a);
+    l = tf32_rna(__fsub_rn(a, h));
+}
+
+__device__ __forceinline__ void producers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(bytes));
+}
+
+// 1-D bulk async copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// hi = the fp32 value itself (the tensor core reads the top 19 bits of a kind::tf32 operand, i.e.
+// truncates), lo = a - trunc_tf32(a) (exact; its own low bits are truncated again by the MMA):
+// two instructions per element instead of rna/sub/rna.
+__device__ __forceinline__ float lo_of(float a) { return __fsub_rn(a, __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
+
+template <class Op>
+__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int tiles) {
+    extern __shared__ __align__(1024) char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+    uint64_t* empty = full + kStages;
+    uint64_t* accf = empty + kStages;
+    uint64_t* acce = accf + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+    const SlotView v = slot_view(p, p.slots[blockIdx.z]);
+    Op op;
+    op.setup(p, v, blockIdx.x);
+    const int M = op.M, N = op.N, K = op.K;
+    const int tile0 = blockIdx.y * tiles;
+    const int ntiles = min(tiles, (M + kBM - 1) / kBM - tile0);
+    if (ntiles <= 0 || K <= 0) return;
+    const int nt = (N + 15) / 16 * 16;
+    const int lbo = nt * 16;  // B canonical: (row r, k) at (k/4)*lbo + (r/8)*128 + (r%8)*16 + (k%4)*4
+    const int nchunks = (K + kKC - 1) / kKC;
+    const int total = ntiles * nchunks;
+    const int klim = op.kbeg + K;
+    const int seg = Op::kSegChunks;  // 0: one accumulation unit per tile
+    const int nseg = seg > 0 ? (nchunks + seg - 1) / seg : 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kWsTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], kProducers + (Op::B_IMAGE ? 1 : 0));
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&accf[a], 1);
+            mbar_init(&acce[a], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kEpiWarp0) {
+        // ================= producers =================
+        const int q = warp & 3, h = warp >> 2;  // TMEM lane quadrant, k half
+        const int pt = threadIdx.x;             // 0..255
+        const uint32_t araw = smem_u32(smem + kStages * kBStage);
+        // K-contiguous A: coalesced cp.async of the raw tile (8 consecutive threads = one row's
+        // 128 bytes), 3 deep; each thread then reads its own row back from shared memory.
+        // this thread's cp.async units: rows pt/8 + 32 j (j < 4), k-quad pt % 8; the rows' decode
+        // (sample, window origin) is computed once per tile
+        typename Op::RowInfo ri[4];
+        int ri_tile = -1;
+        auto a_issue = [&](int gg) {
+            if constexpr (Op::AM == 0) {
+                const int ti = gg / nchunks;
+                const int mm0 = (tile0 + ti) * kBM, kk0 = op.kbeg + (gg % nchunks) * kKC;
+                if (ti != ri_tile) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ri[j] = op.row_info(mm0 + (pt >> 3) + 32 * j);
+                    ri_tile = ti;
+                }
+                const uint32_t dst = araw + (gg % kARaw) * kARawTile;
+                const int kq = pt & 7, k = kk0 + kq * 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = (pt >> 3) + 32 * j;
+                    const float* src = op.a_ptr_ri(ri[j], k);
+                    cp16(dst + (r * kRawLdK + kq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
+                }
+            } else {
+                // MN-contiguous A: unit (row quad pt % 32, reduction k = pt / 32 + 8 j): 16 bytes =
+                // 4 consecutive rows at one k; a warp covers 512 contiguous bytes
+                const int ti = gg / nchunks;
+                const int mm0 = (tile0 + ti) * kBM, kk0 = op.kbeg + (gg % nchunks) * kKC;
+                const int rq = pt & 31;
+                if (ti != ri_tile) {
+                    ri[0] = op.row_info(mm0 + rq * 4);
+                    ri_tile = ti;
+                }
+                const uint32_t dst = araw + (gg % kARaw) * kARawTile;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int k = (pt >> 5) + 8 * j;
+                    const float* src = op.a_ptr_ri(ri[0], kk0 + k);
+                    cp16(dst + (k * kRawLdMN + rq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
+                }
+            }
+            asm volatile("cp.async.commit_group;");
+        };
+        a_issue(0);
+        if (total > 1) a_issue(1);
+        int g = 0;
+        for (int i = 0; i < ntiles; ++i) {
+            const int m0 = (tile0 + i) * kBM;
+            const int m = m0 + q * 32 + lane;
+            const bool mrow = Op::kOnesRow >= 0 ? (m < Op::kOnesRow) : (m < M);
+            for (int c = 0; c < nchunks; ++c, ++g) {
+                const int s = g % kStages, u = g / kStages;
+                const int k0 = op.kbeg + c * kKC;
+                const int ka = k0 + h * 16;
+                // B units: BMODE 0 -> (row, k-quad), consecutive threads = consecutive rows;
+                // BMODE 1 -> (row-quad, k-quad), 4 rows x 4 k transposed in registers
+                float4 b[4];
+                int bunits = 0;
+                if constexpr (Op::B_IMAGE) {
+                } else if constexpr (Op::BMODE == 0) {
+                    bunits = (nt * kKQ + kProducers - 1) / kProducers;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
+                        b[j] = ld4(j < bunits && kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
+                    }
+                } else {
+                    const int rq = pt % 32, kq = pt / 32;  // 32 row-quads x 8 k-quads
+                    bunits = 1;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int k = k0 + kq * 4 + j;
+                        b[j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
+                    }
+                }
+                float a[16];
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // own copies of chunk g landed
+                producers_sync();                                    // everyone's; chunk g-1 consumed
+                if (g + 2 < total) a_issue(g + 2); else asm volatile("cp.async.commit_group;");
+                const char* rawg = smem + kStages * kBStage + (g % kARaw) * kARawTile;
+                if constexpr (Op::AM == 0) {
+                    const float4* rp = reinterpret_cast<const float4*>(rawg + ((q * 32 + lane) * kRawLdK + h * 16) * 4);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float4 t = rp[j];
+                        a[4 * j] = t.x; a[4 * j + 1] = t.y; a[4 * j + 2] = t.z; a[4 * j + 3] = t.w;
+                    }
+                } else {
+                    const float* rp = reinterpret_cast<const float*>(rawg) + (h * 16) * kRawLdMN + q * 32 + lane;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) a[j] = rp[j * kRawLdMN];
+                }
+                (void)mrow;
+                if (Op::kOnesRow >= 0 && m == Op::kOnesRow) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) a[j] = ka + j < klim ? 1.0f : 0.0f;
+                }
+                // ---- wait until the MMAs of this stage's previous use are done
+                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                char* bh = smem + s * kBStage;
+                char* bl = bh + nt * 128;
+                if constexpr (Op::B_IMAGE) {
+                    if (pt == 0) {  // the weight image of this chunk: one bulk copy of hi | lo
+                        mbar_arrive_expect_tx(&full[s], nt * 256);
+                        bulk_g2s(bh, op.b_image(c), nt * 256, &full[s]);
+                    }
+                }
+                // A hi/lo -> TMEM
+                {
+                    float lo[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) lo[j] = lo_of(a[j]);
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kABase + s * 64 + h * 16;
+                    tmem_st16(ta, a);
+                    if (!Op::A_EXACT) tmem_st16(ta + 32, lo);
+                }
+                // B hi/lo -> smem canonical
+                if constexpr (Op::B_IMAGE) {
+                } else if constexpr (Op::BMODE == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt;
+                        if (j < bunits && kq < kKQ) {
+                            const uint32_t off = kq * lbo + (r >> 3) * 128 + (r & 7) * 16;
+                            *reinterpret_cast<float4*>(bh + off) = b[j];
+                            *reinterpret_cast<float4*>(bl + off) =
+                                make_float4(lo_of(b[j].x), lo_of(b[j].y), lo_of(b[j].z), lo_of(b[j].w));
+                        }
+                    }
+                } else {
+                    const int rq = pt % 32, kq = pt / 32;
+                    if (rq * 4 < nt) {
+                        const float blk[4][4] = {{b[0].x, b[1].x, b[2].x, b[3].x},
+                                                 {b[0].y, b[1].y, b[2].y, b[3].y},
+                                                 {b[0].z, b[1].z, b[2].z, b[3].z},
+                                                 {b[0].w, b[1].w, b[2].w, b[3].w}};
+#pragma unroll
+                        for (int ii = 0; ii < 4; ++ii) {
+                            const int jj = (ii + (rq >> 1)) & 3;
+                            const int r = rq * 4 + jj;
+                            const uint32_t off = kq * lbo + (r >> 3) * 128 + (r & 7) * 16;
+                            *reinterpret_cast<float4*>(bh + off) =
+                                make_float4(blk[jj][0], blk[jj][1], blk[jj][2], blk[jj][3]);
+                            *reinterpret_cast<float4*>(bl + off) = make_float4(lo_of(blk[jj][0]), lo_of(blk[jj][1]),
+                                                                               lo_of(blk[jj][2]), lo_of(blk[jj][3]));
+                        }
+                    }
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;");
+                asm volatile("fence.proxy.async.shared::cta;");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                mbar_arrive(&full[s]);
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else if (warp == kMmaWarp) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32(nt);
+            const uint32_t smem_base = smem_u32(smem);
+            int g = 0, un = 0;
+            for (int i = 0; i < ntiles; ++i) {
+                uint32_t dacc = 0;
+                int acc_i = 0;
+                for (int c = 0; c < nchunks; ++c, ++g) {
+                    const bool unit_start = c == 0 || (seg > 0 && c % seg == 0);
+                    const bool unit_end = c == nchunks - 1 || (seg > 0 && c % seg == seg - 1);
+                    if (unit_start) {
+                        acc_i = un & 1;
+                        const int use = un >> 1;
+                        if (use > 0) mbar_wait(&acce[acc_i], (use - 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        dacc = tmem + acc_i * kAcc;
+                    }
+                    const int s = g % kStages, u = g / kStages;
+                    mbar_wait(&full[s], u & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
+                    const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
+                    const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
+                    for (int st = 0; st < ksteps; ++st) {
+                        const uint32_t o = st * 2 * lbo;
+                        const uint64_t dbh = smem_desc(bhi + o, lbo, 128), dbl = smem_desc(blo + o, lbo, 128);
+                        uint32_t accum = (unit_start && st == 0) ? 0u : 1u;
+                        if (!Op::A_EXACT) {
+                            mma_ts(dacc, alo + st * 8, dbh, idesc, accum);
+                            accum = 1u;
+                        }
+                        if (!Op::B_EXACT) {
+                            mma_ts(dacc, ahi + st * 8, dbl, idesc, accum);
+                            accum = 1u;
+                        }
+                        mma_ts(dacc, ahi + st * 8, dbh, idesc, accum);
+                    }
+                    mma_commit(&empty[s]);
+                    if (unit_end) {
+                        mma_commit(&accf[acc_i]);
+                        ++un;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue =================
+        const int q = warp & 3;
+        float4* sacc = reinterpret_cast<float4*>(smem + kWsSmem);  // [col/4][row], segmented Ops only
+        const int row = q * 32 + lane;
+        int un = 0;
+        for (int i = 0; i < ntiles; ++i) {
+            const int m = (tile0 + i) * kBM + row;
+            const bool live = m < M;
+            if (Op::kSegChunks > 0) {
+                // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
+                for (int j = 0; j < nseg; ++j, ++un) {
+                    const int acc_i = un & 1, use = un >> 1;
+                    mbar_wait(&accf[acc_i], use & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    for (int c0 = 0; c0 < nt; c0 += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;");
+                        if (c0 + 16 >= nt) {
+                            asm volatile("tcgen05.fence::before_thread_sync;");
+                            mbar_arrive(&acce[acc_i]);
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < 16; jj += 4) {
+                            float4* sp = sacc + ((c0 + jj) >> 2) * kBM + row;
+                            const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
+                                                          __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
+                            if (j == 0) {
+                                *sp = nv;
+                            } else {
+                                float4 o = *sp;
+                                o.x = __fadd_rn(o.x, nv.x);
+                                o.y = __fadd_rn(o.y, nv.y);
+                                o.z = __fadd_rn(o.z, nv.z);
+                                o.w = __fadd_rn(o.w, nv.w);
+                                *sp = o;
+                            }
+                        }
+                    }
+                }
+            }
+            int acc_i = 0;
+            if (Op::kSegChunks == 0) {
+                acc_i = un & 1;
+                const int use = un >> 1;
+                ++un;
+                mbar_wait(&accf[acc_i], use & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+            for (int c0 = 0; c0 < nt; c0 += 16) {
+                uint32_t r[16];
+                if (Op::kSegChunks > 0) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj += 4) {
+                        const float4 t = sacc[((c0 + jj) >> 2) * kBM + row];
+                        r[jj] = __float_as_uint(t.x); r[jj + 1] = __float_as_uint(t.y);
+                        r[jj + 2] = __float_as_uint(t.z); r[jj + 3] = __float_as_uint(t.w);
+                    }
+                } else {
+                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;");
+                    if (c0 + 16 >= nt) {
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        mbar_arrive(&acce[acc_i]);  // accumulator free for unit un + 1
+                    }
+                }
+                if (!live) continue;
+#pragma unroll
+                for (int j0 = 0; j0 < 16; j0 += 4) {
+                    const int n0 = c0 + j0;
+                    if (n0 >= N) continue;
+                    float x[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j0 + j]);
+                    if constexpr (Op::EPI == ctc::kEpiBiasRelu) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float t = __fadd_rn(x[j], __ldg(op.bias + n0 + j));
+                            x[j] = t > 0.0f ? t : 0.0f;
+                        }
+                        *reinterpret_cast<float4*>(op.c_row(m) + n0) = make_float4(x[0], x[1], x[2], x[3]);
+                    } else if constexpr (Op::EPI == ctc::kEpiMask) {
+                        const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_row(m) + n0));
+                        *reinterpret_cast<float4*>(op.c_row(m) + n0) =
+                            make_float4(mk.x > 0.0f ? x[0] : 0.0f, mk.y > 0.0f ? x[1] : 0.0f,
+                                        mk.z > 0.0f ? x[2] : 0.0f, mk.w > 0.0f ? x[3] : 0.0f);
+                    } else {
+                        float* ptp = op.part + (long long)op.split * N * Op::kPartLd + m;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) ptp[(long long)(n0 + j) * Op::kPartLd] = x[j];
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kWsTmemCols));
+}
+
+}  // namespace ws
+}  // namespace cnn
+}  // namespace smx

@@ -23,6 +23,7 @@
 #include "kernels/gemm_tc.cuh"
 #include "kernels/step_kernels.cuh"
 #include "kernels/cnn.cuh"
+#include "kernels/conv_ws.cuh"
 
 using namespace smx;
 
@@ -199,7 +200,9 @@ constexpr int conv_tpc() {
 template <>
 constexpr int conv_tpc<cnn::ctc::Fwd<1>>() { return 8; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 2; }
+constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 4; }
+template <>
+constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 2; }
 template <>
 constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 4; }
 template <>
@@ -209,21 +212,26 @@ template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
     static bool configured = false;
     if (!configured) {
-        ck(cudaFuncSetAttribute(cnn::ctc::conv_tc_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cnn::ctc::kConvSmem),
+        ck(cudaFuncSetAttribute(cnn::ws::conv_ws_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cnn::ws::ws_smem<Op>()),
            "conv smem attribute");
         configured = true;
     }
     constexpr int tpc = conv_tpc<Op>();
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
     dim3 grid(gx, (mtiles + tpc - 1) / tpc, groups);
-    cnn::ctc::conv_tc_kernel<Op><<<grid, tc3::kThreads, cnn::ctc::kConvSmem, c->cur>>>(a, tpc);
-    launch_check(c, "conv_tc");
+    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::kWsThreads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, tpc);
+    launch_check(c, "conv_ws");
 }
 
 template <int L>
 void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
+    if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
+        cnn::conv1_fwd_fast<<<dim3((mb * 1024 + 255) / 256, n), 256, 0, c->cur>>>(a);
+        launch_check(c, "conv1_fwd_fast");
+        return;
+    }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
         conv_tc<cnn::ctc::Fwd<L>>(c, a, 1, mb * G::OH * G::OH, n);
         return;
@@ -236,6 +244,13 @@ void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
 template <int L>
 void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
+    if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
+        cnn::conv1_wgrad_fast<<<dim3(mb, n), 256, 0, c->cur>>>(a);
+        launch_check(c, "conv1_wgrad_fast");
+        cnn::conv1_wgrad_reduce<<<n, 256, 0, c->cur>>>(a);
+        launch_check(c, "conv1_wgrad_reduce");
+        return;
+    }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
         const int splits = (mb * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
         conv_tc<cnn::ctc::Wgrad<L>>(c, a, splits, cnn::Part<L>::Rows, n);
@@ -259,6 +274,20 @@ void conv_dgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     launch_check(c, "conv_dgrad_simt");
 }
 
+// Pre-split tf32 hi/lo weight images of the three convs (tensor-core mode), see cnn::WImg.
+void weight_images(smx_ctx* c, const cnn::ConvArgs& a, int n) {
+    if (c->d.gemm_mode != SMX_GEMM_TC) return;
+    auto blocks = [](int units) { return (unsigned)((units + 255) / 256); };
+    cnn::weight_image_kernel<1><<<dim3(blocks(cnn::WImg<1>::FwdChunks * 8 * 32), n), 256, 0, c->cur>>>(a);
+    launch_check(c, "weight_image 1");
+    cnn::weight_image_kernel<2><<<dim3(blocks((cnn::WImg<2>::FwdChunks + cnn::WImg<2>::DgrChunks) * 8 * 64), n), 256, 0,
+                                   c->cur>>>(a);
+    launch_check(c, "weight_image 2");
+    cnn::weight_image_kernel<3><<<dim3(blocks((cnn::WImg<3>::FwdChunks + cnn::WImg<3>::DgrChunks) * 8 * 128), n), 256,
+                                   0, c->cur>>>(a);
+    launch_check(c, "weight_image 3");
+}
+
 // One lockstep of the CNN over `n` slots: forward, head, backward as two branches (input
 // gradients on the main stream, weight gradients on the side stream), K5 update, advance.
 void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
@@ -266,6 +295,7 @@ void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
     const cnn::ConvArgs a = cnn_args(c, d_slots);
     StepCtx sc = step_ctx(c, d_slots);
     c->cur = c->stream;
+    weight_images(c, a, n);
     conv_forward<1>(c, a, n, mb);
     conv_forward<2>(c, a, n, mb);
     conv_forward<3>(c, a, n, mb);
@@ -320,6 +350,7 @@ void eval_cnn(smx_ctx* c, int k) {
     a.zout = c->zval;
     a.z_stride = (long long)nv * cnn::kNCP;
     c->cur = c->stream;
+    weight_images(c, a, k);
     for (int r0 = 0; r0 < nv; r0 += mb) {
         a.x_row0 = r0;
         conv_forward<1>(c, a, k, mb);
@@ -605,7 +636,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             c->al = cnn::act_layout(d.max_batch);
             c->act_stride = c->al.stride;
             c->d_in = cnn::kSample;
-            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 16 : 13;
+            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 19 : 13;
         }
         try {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
@@ -1090,6 +1121,7 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
             const cnn::ConvArgs a = cnn_args(c, c->scratch_slots);
             c->cur = c->stream;
+            weight_images(c, a, n);
             auto launch = [&] {
                 if (kind == 2)
                     conv_forward<2>(c, a, n, c->d.max_batch);
