@@ -402,7 +402,7 @@ def main():
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=16),
         }
         roofline = dict(kernels["K1_conv2_fwd"])
-        roofline["kernel"] = ("conv_tc_kernel<Fwd<2>> (conv2 implicit GEMM, 64 groups x M 32768 x N 64 x K 288)"
+        roofline["kernel"] = ("conv_ws_kernel<Fwd<2>> (conv2 implicit GEMM, 64 groups x M 32768 x N 64 x K 288)"
                               if gemm_mode == ex.GEMM_TC else "conv_fwd_simt<2>")
     else:
         kernels = {

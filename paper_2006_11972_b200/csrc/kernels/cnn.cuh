@@ -72,8 +72,12 @@ template <int L>
 struct WImg {
     static constexpr int FwdChunks = (9 * Geo<L>::Ci + 31) / 32;
     static constexpr int FwdFloats = FwdChunks * Geo<L>::Co * 64;
-    static constexpr int DgrChunks = 9 * Geo<L>::Co / 32;
-    static constexpr int DgrFloats = DgrChunks * Geo<L>::Ci * 64;
+    // input gradient as a sub-pixel GEMM: N = 4 parity classes x Ci (in tiles of <= 128 rows),
+    // K = 2x2 output neighbourhood x Co
+    static constexpr int DgrN = 4 * Geo<L>::Ci;
+    static constexpr int DgrNTile = DgrN < 128 ? DgrN : 128;
+    static constexpr int DgrChunks = 4 * Geo<L>::Co / 32;
+    static constexpr int DgrFloats = DgrChunks * DgrN * 64;
     // first chunk of parity class c (taps 1, 2, 2, 4)
     static __host__ __device__ constexpr int class_chunk0(int c) {
         return (c == 0 ? 0 : c == 1 ? 1 : c == 2 ? 3 : 5) * Geo<L>::Co / 32;
@@ -459,7 +463,7 @@ __device__ __align__(16) float kZero16[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 template <int L>
 struct Fwd {
     using G = Geo<L>;
-    static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu;
+    static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
     const float* in;
@@ -505,86 +509,71 @@ struct Fwd {
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
     __device__ __forceinline__ float* c_row(int m) const { return out + (long long)m * G::Co; }
+    __device__ __forceinline__ float* c_at(int m, int col) const { return out + (long long)m * G::Co + col; }
     __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
+    __device__ __forceinline__ const float* mask_at(int, int) const { return nullptr; }
 };
 
-// Input gradient of a stride-2 layer for one parity class (ih % 2, iw % 2) = (pi, pj):
-// rows r = (n, a, b) -> input pixel (2a + pi, 2b + pj); K = (dense tap j of the class, co).
+// Input gradient of a stride-2 layer as one dense "sub-pixel" GEMM: row r = (n, a, b) stands
+// for the 2x2 input block (2a + pi, 2b + pj), column = (class pi*2+pj, ci), reduction k =
+// (output neighbour (a + da, b + db), co).  An input pixel of class (pi, pj) receives tap
+// kh = (pi ? (da ? 0 : 2) : 1) from output row a + da (da = 0 only for pi = 0), likewise kw, so
+// B[(cls, ci)][(da, db, co)] = W[co][kh][kw][ci] or 0: 9 of the 16 (class, neighbour) pairs are
+// taps.  Versus one GEMM per parity class this gathers each output-gradient block once for 4
+// input pixels (4/9 of the gather work) with N = 4 Ci instead of Ci.
+// blockIdx.x selects the 128-column half of N when 4 Ci > 128.
 template <int L>
 struct Dgrad {
     using G = Geo<L>;
-    static_assert(G::S == 2, "parity decomposition is for stride 2");
-    static constexpr int AM = 0, BMODE = 1, EPI = kEpiMask;
+    static_assert(G::S == 2, "sub-pixel decomposition is for stride 2");
+    static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
-    static constexpr int HH = G::H / 2;
+    static constexpr int HH = G::H / 2;  // == OH
     const float* dy;
     const float* w;
     const float* act;
     float* dx;
     const float* img;
     int M, N, K, kbeg, m0, split;
-    int pi, pj, nkw;  // class, taps per row of the class
+    int col0;  // first (class, ci) column of this N tile
     struct RowInfo {
-        int base, ih, iw;  // sample offset in dy, input pixel (-1000: invalid row)
+        int base, a, b;  // sample offset in dy, block coordinates (a = -1000: invalid row)
     };
-    __device__ void setup(const ConvArgs& p, const SlotView& v, int cls) {
-        img = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)WImg<L>::class_chunk0(cls) * G::Ci * 64;
+    __device__ void setup(const ConvArgs& p, const SlotView& v, int half) {
         dy = layer_dout<L>(p, v);
         w = v.w + G::OffW;
         act = layer_out<L - 1>(p, v);
         dx = layer_dout<L - 1>(p, v);
-        pi = cls >> 1;
-        pj = cls & 1;
-        const int nkh = pi ? 2 : 1;
-        nkw = pj ? 2 : 1;
+        N = WImg<L>::DgrNTile;
+        col0 = half * N;
+        img = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)half * WImg<L>::DgrChunks * N * 64;
         M = v.bs * HH * HH;
-        N = G::Ci;
-        K = nkh * nkw * G::Co;
+        K = 4 * G::Co;
         kbeg = 0;
         split = 0;
-    }
-    __device__ __forceinline__ void tap(int j, int& kh, int& kw) const {
-        const int jh = j / nkw, jw = j % nkw;
-        kh = pi ? 2 * jh : 1;
-        kw = pj ? 2 * jw : 1;
     }
     __device__ __forceinline__ RowInfo row_info(int r) const {
         if (r >= M) return RowInfo{0, -1000, -1000};
         const int n = r / (HH * HH), q = r % (HH * HH);
-        return RowInfo{n * G::OH * G::OH * G::Co, 2 * (q / HH) + pi, 2 * (q % HH) + pj};
+        return RowInfo{n * G::OH * G::OH * G::Co, q / HH, q % HH};
     }
     __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& ri, int k) const {
-        int kh, kw;
-        tap(k / G::Co, kh, kw);
-        const int nh = ri.ih + 1 - kh, nw = ri.iw + 1 - kw;  // even by the class parity
-        const int oh = nh >> 1, ow = nw >> 1;
-        if (nh < 0 || nw < 0 || oh >= G::OH || ow >= G::OH || k >= K) return nullptr;
-        return dy + ri.base + (oh * G::OH + ow) * G::Co + k % G::Co;
+        const int nb = k / G::Co, co = k % G::Co;  // neighbour (da, db) = (nb >> 1, nb & 1)
+        const int oh = ri.a + (nb >> 1), ow = ri.b + (nb & 1);
+        if ((unsigned)oh >= (unsigned)G::OH || (unsigned)ow >= (unsigned)G::OH) return nullptr;
+        return dy + ri.base + (oh * G::OH + ow) * G::Co + co;
     }
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
-    __device__ __forceinline__ long long pix_off(int r) const {
+    // epilogue column c (0..N-1) -> (class, ci); rows write 4 input pixels
+    __device__ __forceinline__ long long pix_off(int r, int col) const {
+        const int cc = col0 + col, cls = cc / G::Ci;
         const int n = r / (HH * HH), q = r % (HH * HH);
-        const int ih = 2 * (q / HH) + pi, iw = 2 * (q % HH) + pj;
-        return (((long long)n * G::H + ih) * G::H + iw) * G::Ci;
+        const int ih = 2 * (q / HH) + (cls >> 1), iw = 2 * (q % HH) + (cls & 1);
+        return (((long long)n * G::H + ih) * G::H + iw) * G::Ci + cc % G::Ci;
     }
-    __device__ __forceinline__ const float* a_ptr(int r, int k) const {
-        const int n = r / (HH * HH), q = r % (HH * HH);
-        const int ih = 2 * (q / HH) + pi, iw = 2 * (q % HH) + pj;
-        int kh, kw;
-        tap(k / G::Co, kh, kw);
-        const int oh = (ih + 1 - kh) >> 1, ow = (iw + 1 - kw) >> 1;  // parity makes these exact
-        if (ih + 1 - kh < 0 || iw + 1 - kw < 0 || oh >= G::OH || ow >= G::OH) return nullptr;
-        return dy + (((long long)n * G::OH + oh) * G::OH + ow) * G::Co + k % G::Co;
-    }
-    // B(row = ci, k = (j, co)) = W[co][t(j)][ci]; 4 consecutive ci are contiguous
-    __device__ __forceinline__ const float* b_ptr(int ci, int k) const {
-        int kh, kw;
-        tap(k / G::Co, kh, kw);
-        return w + ((long long)(k % G::Co) * 9 + kh * 3 + kw) * G::Ci + ci;
-    }
-    __device__ __forceinline__ float* c_row(int r) const { return dx + pix_off(r); }
-    __device__ __forceinline__ const float* mask_row(int r) const { return act + pix_off(r); }
+    __device__ __forceinline__ float* c_at(int r, int col) const { return dx + pix_off(r, col); }
+    __device__ __forceinline__ const float* mask_at(int r, int col) const { return act + pix_off(r, col); }
 };
 
 // Weight gradient, split s of the reduction: part[s][co][k] = sum_{m in split} im2col(in)[m][k] dy[m][co]
@@ -592,7 +581,7 @@ struct Dgrad {
 template <int L>
 struct Wgrad {
     using G = Geo<L>;
-    static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT;
+    static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false;
     struct RowInfo {
         int kh, kw, ci;  // tap and first channel of a row quad (kh = -1000: padding rows)
@@ -637,7 +626,9 @@ struct Wgrad {
     }
     __device__ __forceinline__ const float* b_ptr(int co, int m) const { return dy + (long long)m * G::Co + co; }
     __device__ __forceinline__ float* c_row(int) const { return nullptr; }
+    __device__ __forceinline__ float* c_at(int, int) const { return nullptr; }
     __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
+    __device__ __forceinline__ const float* mask_at(int, int) const { return nullptr; }
 };
 
 // cp.async of one operand tile through an address functor (16-byte units, zero fill).
@@ -864,7 +855,7 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* W = v.w + G::OffW;
     const int fwd_units = WImg<L>::FwdChunks * 8 * G::Co;
-    const int dgr_units = (L >= 2) ? WImg<L>::DgrChunks * 8 * G::Ci : 0;
+    const int dgr_units = (L >= 2) ? WImg<L>::DgrChunks * 8 * WImg<L>::DgrN : 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < fwd_units + dgr_units; u += gridDim.x * blockDim.x) {
         float val[4];
         float* dst;
@@ -879,23 +870,25 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
             }
             dst = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3) + (long long)c * nt * 64 +
                   (kq * nt * 16 + (r >> 3) * 128 + (r & 7) * 16) / 4;
-        } else {  // rows ci, per class k = (dense tap j, co)
+        } else {  // rows (class, ci), k = (neighbour (da, db), co)
             const int uu = u - fwd_units;
-            nt = G::Ci;
-            const int cg = uu / (8 * nt), kq = (uu / nt) % 8, r = uu % nt;
-            int cls = 0;
-            while (cls < 3 && cg >= WImg<L>::class_chunk0(cls + 1)) ++cls;
-            const int c = cg - WImg<L>::class_chunk0(cls);
-            const int pi = cls >> 1, pj = cls & 1, nkw = pj ? 2 : 1;
+            constexpr int NT = WImg<L>::DgrNTile;
+            const int half = uu / (WImg<L>::DgrChunks * 8 * NT);
+            const int rem = uu % (WImg<L>::DgrChunks * 8 * NT);
+            const int c = rem / (8 * NT), kq = (rem / NT) % 8, r = rem % NT;
+            nt = NT;
+            const int cc = half * NT + r, cls = cc / G::Ci, ci = cc % G::Ci;
+            const int pi = cls >> 1, pj = cls & 1;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int k = c * 32 + kq * 4 + e;
-                const int j = k / G::Co, co = k % G::Co;
-                const int kh = pi ? 2 * (j / nkw) : 1, kw = pj ? 2 * (j % nkw) : 1;
-                val[e] = W[(co * 9 + kh * 3 + kw) * G::Ci + r];
+                const int nb = k / G::Co, co = k % G::Co, da = nb >> 1, db = nb & 1;
+                const int kh = pi ? (da ? 0 : 2) : (da ? -1 : 1);
+                const int kw = pj ? (db ? 0 : 2) : (db ? -1 : 1);
+                val[e] = (kh >= 0 && kw >= 0) ? W[(co * 9 + kh * 3 + kw) * G::Ci + ci] : 0.0f;
             }
-            dst = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)cg * nt * 64 +
-                  (kq * nt * 16 + (r >> 3) * 128 + (r & 7) * 16) / 4;
+            dst = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)half * WImg<L>::DgrChunks * NT * 64 +
+                  (long long)c * NT * 64 + (kq * NT * 16 + (r >> 3) * 128 + (r & 7) * 16) / 4;
         }
         float4 hi, lo;
         hi.x = tf32_rna_h(val[0]); lo.x = tf32_rna_h(__fsub_rn(val[0], hi.x));
@@ -918,14 +911,15 @@ __global__ void __launch_bounds__(256) conv1_fwd_fast(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     __shared__ __align__(16) float wt[27][32];
     __shared__ float bs_[32];
+    __shared__ __align__(16) float stage[256 * 36];  // 256 pixels x (32 + 4 pad) floats
     for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
         const int co = i & 31, k = i >> 5, t = k / 3, ci = k % 3;
         wt[k][co] = v.w[Geo<1>::OffW + (co * 9 + t) * 4 + ci];
     }
     if (threadIdx.x < 32) bs_[threadIdx.x] = v.w[Geo<1>::OffB + threadIdx.x];
     __syncthreads();
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= v.bs * 1024) return;
+    if (blockIdx.x * blockDim.x >= v.bs * 1024) return;
+    const int m = min(blockIdx.x * blockDim.x + threadIdx.x, v.bs * 1024 - 1);  // tail threads recompute
     const float* in = layer_in<1>(p, v);
     const int n = m >> 10, oh = (m >> 5) & 31, ow = m & 31;
     float acc[32];
@@ -950,11 +944,19 @@ __global__ void __launch_bounds__(256) conv1_fwd_fast(ConvArgs p) {
             }
         }
     }
-    float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)m * 32);
+    // stage the block's 256 x 32 outputs in shared memory (row stride 33 float4-quads... padded) and
+    // write them back as contiguous 16-byte stores
+    __syncthreads();  // wt no longer needed: reuse nothing, stage separately
+    float4* st = reinterpret_cast<float4*>(stage) + threadIdx.x * 9;
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4)
-        out[c4] = make_float4(fmaxf(acc[4 * c4], 0.0f), fmaxf(acc[4 * c4 + 1], 0.0f), fmaxf(acc[4 * c4 + 2], 0.0f),
-                              fmaxf(acc[4 * c4 + 3], 0.0f));
+        st[c4] = make_float4(fmaxf(acc[4 * c4], 0.0f), fmaxf(acc[4 * c4 + 1], 0.0f), fmaxf(acc[4 * c4 + 2], 0.0f),
+                             fmaxf(acc[4 * c4 + 3], 0.0f));
+    __syncthreads();
+    const int m_first = blockIdx.x * blockDim.x;
+    const int rows = min((int)blockDim.x, v.bs * 1024 - m_first);
+    float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)m_first * 32);
+    for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) out[i] = reinterpret_cast<float4*>(stage)[(i >> 3) * 9 + (i & 7)];
 }
 
 // Per-sample partial weight gradient of conv1: block = one (sample, slot); lane = output channel,
@@ -980,17 +982,23 @@ __global__ void __launch_bounds__(256) conv1_wgrad_fast(ConvArgs p) {
     float acc[28];
 #pragma unroll
     for (int j = 0; j < 28; ++j) acc[j] = 0.0f;
-    for (int pix = warp * 128; pix < warp * 128 + 128; ++pix) {
-        const float d = dy[pix * 32 + co];
-        const int oh = pix >> 5, ow = pix & 31;
+    for (int p0 = warp * 128; p0 < warp * 128 + 128; p0 += 8) {
+        float dv[8];
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            const float4 x = reinterpret_cast<const float4*>(img)[(oh + t / 3) * 34 + ow + t % 3];
-            acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
-            acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
-            acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
+        for (int e = 0; e < 8; ++e) dv[e] = __ldg(dy + (p0 + e) * 32 + co);  // 8 loads in flight
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int pix = p0 + e, oh = pix >> 5, ow = pix & 31;
+            const float d = dv[e];
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+                const float4 x = reinterpret_cast<const float4*>(img)[(oh + t / 3) * 34 + ow + t % 3];
+                acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
+                acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
+                acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
+            }
+            acc[27] = __fadd_rn(acc[27], d);
         }
-        acc[27] = __fadd_rn(acc[27], d);
     }
 #pragma unroll
     for (int j = 0; j < 28; ++j) red[warp][co * 28 + j] = acc[j];

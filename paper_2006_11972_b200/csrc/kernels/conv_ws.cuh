@@ -32,21 +32,35 @@ namespace ws {
 
 using namespace smx::tc3;
 
-constexpr int kStages = 3;                       // B smem / A TMEM ring
-constexpr int kARaw = 3;                         // producer-side cp.async ring of raw A tiles
+constexpr int kMaxStages = 4;                    // B smem / A TMEM ring (TMEM: 4 x 64 columns)
 constexpr int kProducers = 256;                  // warps 0-7
 constexpr int kEpiWarp0 = 8;                     // warps 8-11
 constexpr int kMmaWarp = 12;
 constexpr int kWsThreads = 13 * 32;
 constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K-major canonical, N <= 128
-constexpr int kBStage = 2 * kBTile;
 constexpr int kARawTile = kBM * kRawLdK * 4;     // raw A tile [128 rows][32 + 4 pad]
-constexpr int kBarOff = kStages * kBStage + kARaw * kARawTile;
-constexpr int kWsSmem = kBarOff + 128;
-constexpr int kSaccBytes = kBM * 128 * 4;        // segment-sum tile, float4 [col/4][row][4]
+
+// Shared-memory plan of one Op, sized by its N (the B tiles and the segment sums scale with it):
+// kStages B stages | kARaw raw A tiles | barriers | segment sums.  The raw-A ring takes what is
+// left of the 227 KB (at most 8 deep): the prefetch distance is kARaw - 1 chunks.
+template <class Op>
+struct WsPlan {
+    static constexpr int N = Op::kMaxN;
+    static constexpr int Stages = N >= 128 ? 3 : kMaxStages;
+    static constexpr int BStage = N * 256;                          // hi + lo tiles
+    static constexpr int Sacc = Op::kSegChunks > 0 ? kBM * N * 4 : 0;
+    static constexpr int Fixed = Stages * BStage + 128 + Sacc;
+    static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
+    static constexpr int ARaw = ARawMax > 8 ? 8 : ARawMax;
+    static_assert(ARaw >= 3, "shared memory plan");
+    static constexpr int ARawOff = Stages * BStage;
+    static constexpr int BarOff = ARawOff + ARaw * kARawTile;
+    static constexpr int SaccOff = BarOff + 128;
+    static constexpr int Bytes = SaccOff + Sacc;
+};
 template <class Op>
 constexpr int ws_smem() {
-    return kWsSmem + (Op::kSegChunks > 0 ? kSaccBytes : 0);
+    return WsPlan<Op>::Bytes;
 }
 constexpr int kWsTmemCols = 512;
 constexpr int kAcc = 128;                        // columns per accumulator
@@ -105,7 +119,10 @@ __device__ __forceinline__ float lo_of(float a) { return __fsub_rn(a, __uint_as_
 template <class Op>
 __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int tiles) {
     extern __shared__ __align__(1024) char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+    using Plan = WsPlan<Op>;
+    constexpr int kBStage = Plan::BStage, kARaw = Plan::ARaw, kPre = Plan::ARaw - 1;  // prefetch distance
+    constexpr int kStages = Plan::Stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Plan::BarOff);
     uint64_t* empty = full + kStages;
     uint64_t* accf = empty + kStages;
     uint64_t* acce = accf + 2;
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
         // ================= producers =================
         const int q = warp & 3, h = warp >> 2;  // TMEM lane quadrant, k half
         const int pt = threadIdx.x;             // 0..255
-        const uint32_t araw = smem_u32(smem + kStages * kBStage);
+        const uint32_t araw = smem_u32(smem + Plan::ARawOff);
         // K-contiguous A: coalesced cp.async of the raw tile (8 consecutive threads = one row's
         // 128 bytes), 3 deep; each thread then reads its own row back from shared memory.
         // this thread's cp.async units: rows pt/8 + 32 j (j < 4), k-quad pt % 8; the rows' decode
@@ -196,9 +213,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
             }
             asm volatile("cp.async.commit_group;");
         };
-        a_issue(0);
-        if (total > 1) a_issue(1);
+        for (int gg = 0; gg < kPre; ++gg) {
+            if (gg < total)
+                a_issue(gg);
+            else
+                asm volatile("cp.async.commit_group;");
+        }
         int g = 0;
+        float4 bn[4];  // next chunk's B registers (non-image Ops)
         for (int i = 0; i < ntiles; ++i) {
             const int m0 = (tile0 + i) * kBM;
             const int m = m0 + q * 32 + lane;
@@ -207,32 +229,39 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                 const int s = g % kStages, u = g / kStages;
                 const int k0 = op.kbeg + c * kKC;
                 const int ka = k0 + h * 16;
-                // B units: BMODE 0 -> (row, k-quad), consecutive threads = consecutive rows;
-                // BMODE 1 -> (row-quad, k-quad), 4 rows x 4 k transposed in registers
+                // B units (register path, non-image Ops): BMODE 0 -> (row, k-quad), consecutive
+                // threads = consecutive rows; BMODE 1 -> (row-quad, k-quad), 4 rows x 4 k transposed
+                // in registers.  Loaded one chunk ahead (bn) so the global latency overlaps a chunk.
+                const int bunits = Op::BMODE == 0 ? (nt * kKQ + kProducers - 1) / kProducers : 1;
+                auto b_load = [&](int kk0, float4* dst) {
+                    if constexpr (Op::B_IMAGE) {
+                    } else if constexpr (Op::BMODE == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt, k = kk0 + kq * 4;
+                            dst[j] = ld4(j < bunits && kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
+                        }
+                    } else {
+                        const int rq = pt % 32, kq = pt / 32;  // 32 row-quads x 8 k-quads
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int k = kk0 + kq * 4 + j;
+                            dst[j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
+                        }
+                    }
+                };
                 float4 b[4];
-                int bunits = 0;
-                if constexpr (Op::B_IMAGE) {
-                } else if constexpr (Op::BMODE == 0) {
-                    bunits = (nt * kKQ + kProducers - 1) / kProducers;
+                if (!Op::B_IMAGE) {
+                    if (g == 0) b_load(k0, bn);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
-                        b[j] = ld4(j < bunits && kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
-                    }
-                } else {
-                    const int rq = pt % 32, kq = pt / 32;  // 32 row-quads x 8 k-quads
-                    bunits = 1;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int k = k0 + kq * 4 + j;
-                        b[j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
-                    }
+                    for (int j = 0; j < 4; ++j) b[j] = bn[j];
+                    if (g + 1 < total) b_load(op.kbeg + ((c + 1 == nchunks) ? 0 : (c + 1)) * kKC, bn);
                 }
                 float a[16];
-                asm volatile("cp.async.wait_group 1;" ::: "memory");  // own copies of chunk g landed
-                producers_sync();                                    // everyone's; chunk g-1 consumed
-                if (g + 2 < total) a_issue(g + 2); else asm volatile("cp.async.commit_group;");
-                const char* rawg = smem + kStages * kBStage + (g % kARaw) * kARawTile;
+                asm volatile("cp.async.wait_group %0;" ::"n"(kPre - 1) : "memory");  // own copies of chunk g landed
+                producers_sync();  // everyone's copies landed; chunk g-1's buffer is consumed
+                if (g + kPre < total) a_issue(g + kPre); else asm volatile("cp.async.commit_group;");
+                const char* rawg = smem + Plan::ARawOff + (g % kARaw) * kARawTile;
                 if constexpr (Op::AM == 0) {
                     const float4* rp = reinterpret_cast<const float4*>(rawg + ((q * 32 + lane) * kRawLdK + h * 16) * 4);
 #pragma unroll
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
     } else {
         // ================= epilogue =================
         const int q = warp & 3;
-        float4* sacc = reinterpret_cast<float4*>(smem + kWsSmem);  // [col/4][row], segmented Ops only
+        float4* sacc = reinterpret_cast<float4*>(smem + Plan::SaccOff);  // [col/4][row], segmented Ops only
         const int row = q * 32 + lane;
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
@@ -437,10 +466,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                             const float t = __fadd_rn(x[j], __ldg(op.bias + n0 + j));
                             x[j] = t > 0.0f ? t : 0.0f;
                         }
-                        *reinterpret_cast<float4*>(op.c_row(m) + n0) = make_float4(x[0], x[1], x[2], x[3]);
+                        *reinterpret_cast<float4*>(op.c_at(m, n0)) = make_float4(x[0], x[1], x[2], x[3]);
                     } else if constexpr (Op::EPI == ctc::kEpiMask) {
-                        const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_row(m) + n0));
-                        *reinterpret_cast<float4*>(op.c_row(m) + n0) =
+                        const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_at(m, n0)));
+                        *reinterpret_cast<float4*>(op.c_at(m, n0)) =
                             make_float4(mk.x > 0.0f ? x[0] : 0.0f, mk.y > 0.0f ? x[1] : 0.0f,
                                         mk.z > 0.0f ? x[2] : 0.0f, mk.w > 0.0f ? x[3] : 0.0f);
                     } else {

@@ -266,7 +266,7 @@ template <int L>
 void conv_dgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC) {
-        conv_tc<cnn::ctc::Dgrad<L>>(c, a, 4, mb * (G::H / 2) * (G::H / 2), n);
+        conv_tc<cnn::ctc::Dgrad<L>>(c, a, cnn::WImg<L>::DgrN / cnn::WImg<L>::DgrNTile, mb * (G::H / 2) * (G::H / 2), n);
         return;
     }
     const long long total = (long long)mb * G::H * G::H * G::Ci;
@@ -280,11 +280,11 @@ void weight_images(smx_ctx* c, const cnn::ConvArgs& a, int n) {
     auto blocks = [](int units) { return (unsigned)((units + 255) / 256); };
     cnn::weight_image_kernel<1><<<dim3(blocks(cnn::WImg<1>::FwdChunks * 8 * 32), n), 256, 0, c->cur>>>(a);
     launch_check(c, "weight_image 1");
-    cnn::weight_image_kernel<2><<<dim3(blocks((cnn::WImg<2>::FwdChunks + cnn::WImg<2>::DgrChunks) * 8 * 64), n), 256, 0,
-                                   c->cur>>>(a);
+    cnn::weight_image_kernel<2><<<dim3(blocks(cnn::WImg<2>::FwdChunks * 8 * 64 + cnn::WImg<2>::DgrChunks * 8 * 128), n),
+                                   256, 0, c->cur>>>(a);
     launch_check(c, "weight_image 2");
-    cnn::weight_image_kernel<3><<<dim3(blocks((cnn::WImg<3>::FwdChunks + cnn::WImg<3>::DgrChunks) * 8 * 128), n), 256,
-                                   0, c->cur>>>(a);
+    cnn::weight_image_kernel<3><<<dim3(blocks(cnn::WImg<3>::FwdChunks * 8 * 128 + cnn::WImg<3>::DgrChunks * 8 * 256), n),
+                                   256, 0, c->cur>>>(a);
     launch_check(c, "weight_image 3");
 }
 
