@@ -393,25 +393,28 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
 }
 
 // grid (groups), block 256: loss = (sum_n rl) / B; gW4[k][c] = fmaf chain over n; gb4[k] = sum_n dz
-__global__ void __launch_bounds__(256) head_grad_kernel(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.x]);
+// grid (17, groups), block 128: one output per thread (the chains are sequential in n, so the
+// parallelism is across outputs; the loads are independent of the chain and unrolled ahead).
+__global__ void __launch_bounds__(128) head_grad_kernel(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* dz = v.act + p.al.dz;
     const float* g = v.act + p.al.g;
     float* gr = p.grad + p.grad_stride * v.slot;
-    for (int i = threadIdx.x; i < kNCP * kFeat + kNCP; i += blockDim.x) {
-        if (i < kNCP * kFeat) {
-            const int k = i / kFeat, c = i % kFeat;
-            float acc = 0.0f;
-            for (int n = 0; n < v.bs; ++n) acc = __fmaf_rn(dz[n * kNCP + k], g[n * kFeat + c], acc);
-            gr[kOffW4 + i] = acc;
-        } else {
-            const int k = i - kNCP * kFeat;
-            float s = 0.0f;
-            for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, dz[n * kNCP + k]);
-            gr[kOffB4 + k] = s;
-        }
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kNCP * kFeat) {
+        const int k = i / kFeat, c = i % kFeat;
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int n = 0; n < v.bs; ++n) acc = __fmaf_rn(__ldg(dz + n * kNCP + k), __ldg(g + n * kFeat + c), acc);
+        gr[kOffW4 + i] = acc;
+    } else if (i < kNCP * kFeat + kNCP) {
+        const int k = i - kNCP * kFeat;
+        float s = 0.0f;
+#pragma unroll 8
+        for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, __ldg(dz + n * kNCP + k));
+        gr[kOffB4 + k] = s;
     }
-    if (threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         float s = 0.0f;
         for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, v.act[p.al.rl + n]);
         p.loss_hist[(long long)v.slot * p.hp_cap + p.st[v.slot].step] = __fdiv_rn(s, (float)v.bs);
@@ -1011,14 +1014,15 @@ __global__ void __launch_bounds__(256) conv1_wgrad_fast(ConvArgs p) {
     }
 }
 
-// Sum the per-sample partials in sample order into the gradient slab.  grid (groups), block 256.
-__global__ void __launch_bounds__(256) conv1_wgrad_reduce(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.x]);
+// Sum the per-sample partials in sample order into the gradient slab.  grid (7, groups), block 128.
+__global__ void __launch_bounds__(128) conv1_wgrad_reduce(ConvArgs p) {
+    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* part = v.act + p.al.w1p;
     float* g = p.grad + p.grad_stride * v.slot;
-    for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kL1Outs; i += gridDim.x * blockDim.x) {
         float s_ = 0.0f;
-        for (int n = 0; n < v.bs; ++n) s_ = __fadd_rn(s_, part[(long long)n * kL1Outs + i]);
+#pragma unroll 8
+        for (int n = 0; n < v.bs; ++n) s_ = __fadd_rn(s_, __ldg(part + (long long)n * kL1Outs + i));
         const int co = i / 28, j = i % 28;
         if (j < 27)
             g[Geo<1>::OffW + (co * 9 + j / 3) * 4 + j % 3] = s_;
@@ -1026,7 +1030,8 @@ __global__ void __launch_bounds__(256) conv1_wgrad_reduce(ConvArgs p) {
             g[Geo<1>::OffB + co] = s_;
     }
     // the padded input channel's weights stay exactly zero
-    for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) g[Geo<1>::OffW + i * 4 + 3] = 0.0f;
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) g[Geo<1>::OffW + i * 4 + 3] = 0.0f;
 }
 
 // Weight-gradient reduction: grad[W][co][k] = sum_{s asc} part[s][co][k] (k < 9 Ci), grad[b][co]

@@ -247,7 +247,7 @@ void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
         cnn::conv1_wgrad_fast<<<dim3(mb, n), 256, 0, c->cur>>>(a);
         launch_check(c, "conv1_wgrad_fast");
-        cnn::conv1_wgrad_reduce<<<n, 256, 0, c->cur>>>(a);
+        cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a);
         launch_check(c, "conv1_wgrad_reduce");
         return;
     }
@@ -301,7 +301,7 @@ void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
     conv_forward<3>(c, a, n, mb);
     cnn::head_fwd_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
     launch_check(c, "head_fwd");
-    cnn::head_grad_kernel<<<n, 256, 0, c->stream>>>(a);
+    cnn::head_grad_kernel<<<dim3((cnn::kNCP * cnn::kFeat + cnn::kNCP + 127) / 128, n), 128, 0, c->stream>>>(a);
     launch_check(c, "head_grad");
     cnn::head_dg_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
     launch_check(c, "head_dg");
@@ -563,6 +563,9 @@ void check_ckpt(smx_ctx* c, int ck_) {
     if (ck_ < 0 || ck_ >= c->C) fail(SMX_ECONFIG, "checkpoint " + std::to_string(ck_) + " out of range");
 }
 
+// blocks per fork job: every thread moves 4 x 16 B per pass (the kernel's unrolled loop)
+unsigned fork_blocks(long long n4) { return (unsigned)std::max<long long>(1, std::min<long long>(148, (n4 + 1023) / 1024)); }
+
 void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
     if (jobs.empty()) return;
     if ((int)jobs.size() > c->jobs_cap) {
@@ -574,7 +577,7 @@ void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
        "jobs H2D");
     const long long n4 = 2 * c->palloc / 4;
     if (c->timing) cudaEventRecord(c->ev[4], c->stream);
-    fork_copy_kernel<<<dim3(148, (unsigned)jobs.size()), 256, 0, c->stream>>>(c->jobs, n4);
+    fork_copy_kernel<<<dim3(fork_blocks(n4), (unsigned)jobs.size()), 256, 0, c->stream>>>(c->jobs, n4);
     launch_check(c, "fork_copy");
     if (c->timing) {
         cudaEventRecord(c->ev[5], c->stream);
@@ -1110,9 +1113,9 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             }
             ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
             const long long n4 = 2 * c->palloc / 4;
-            for (int w = 0; w < 3; ++w) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
+            for (int w = 0; w < 3; ++w) fork_copy_kernel<<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(c->jobs, n4);
             cudaEventRecord(c->ev[6], c->stream);
-            for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(148, n), 256, 0, c->stream>>>(c->jobs, n4);
+            for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(c->jobs, n4);
             cudaEventRecord(c->ev[7], c->stream);
         } else if ((kind == 2 || kind == 3) && c->cnn) {
             if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
