@@ -476,7 +476,8 @@ struct Fwd {
     const float* img;
     int M, N, K, kbeg, m0, split;
     struct RowInfo {
-        int base, ih0, iw0;  // sample offset, top-left input pixel of the 3x3 window (-1: invalid row)
+        const float* ptr;  // input element (top-left of the 3x3 window, channel 0); may be out of range
+        uint32_t vmask;    // bit t: tap t of the window lies inside the image (0 for rows >= M)
     };
     __device__ void setup(const ConvArgs& p, const SlotView& v, int tile_y) {
         img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
@@ -499,15 +500,25 @@ struct Fwd {
         return in + (((long long)n * G::H + ih) * G::H + iw) * G::Ci + ci;
     }
     __device__ __forceinline__ RowInfo row_info(int m) const {
-        if (m >= M) return RowInfo{0, -1000, -1000};
+        if (m >= M) return RowInfo{in, 0u};
         const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
-        return RowInfo{n * G::H * G::H * G::Ci, (pix / G::OH) * G::S - 1, (pix % G::OH) * G::S - 1};
+        const int ih0 = (pix / G::OH) * G::S - 1, iw0 = (pix % G::OH) * G::S - 1;
+        uint32_t mask = 0;
+#pragma unroll
+        for (int t = 0; t < 9; ++t)
+            if ((unsigned)(ih0 + t / 3) < (unsigned)G::H && (unsigned)(iw0 + t % 3) < (unsigned)G::H) mask |= 1u << t;
+        return RowInfo{in + (n * G::H * G::H + ih0 * G::H + iw0) * G::Ci, mask};
     }
-    __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& r, int k) const {
-        const int t = k / G::Ci, ci = k % G::Ci;
-        const int ih = r.ih0 + t / 3, iw = r.iw0 + t % 3;
-        if ((unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H || k >= K) return nullptr;
-        return in + r.base + (ih * G::H + iw) * G::Ci + ci;
+    // per-chunk decode of a producer's k (shared by its 4 rows), then per-row pointer
+    struct TapInfo {
+        int off, bit;  // element offset from the window origin; mask bit (31: k beyond K)
+    };
+    __device__ __forceinline__ TapInfo tap_info(int k) const {
+        const int t = k / G::Ci;
+        return k < K ? TapInfo{((t / 3) * G::H + t % 3) * G::Ci + k % G::Ci, t} : TapInfo{0, 31};
+    }
+    __device__ __forceinline__ const float* a_ptr_tap(const RowInfo& r, const TapInfo& t) const {
+        return (r.vmask >> t.bit) & 1u ? r.ptr + t.off : nullptr;
     }
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
@@ -541,7 +552,8 @@ struct Dgrad {
     int M, N, K, kbeg, m0, split;
     int col0;  // first (class, ci) column of this N tile
     struct RowInfo {
-        int base, a, b;  // sample offset in dy, block coordinates (a = -1000: invalid row)
+        const float* ptr;  // dy at output pixel (a, b), channel 0
+        uint32_t vmask;    // bit 2 da + db: neighbour (a + da, b + db) exists (0 for rows >= M)
     };
     __device__ void setup(const ConvArgs& p, const SlotView& v, int half) {
         dy = layer_dout<L>(p, v);
@@ -557,15 +569,22 @@ struct Dgrad {
         split = 0;
     }
     __device__ __forceinline__ RowInfo row_info(int r) const {
-        if (r >= M) return RowInfo{0, -1000, -1000};
+        if (r >= M) return RowInfo{dy, 0u};
         const int n = r / (HH * HH), q = r % (HH * HH);
-        return RowInfo{n * G::OH * G::OH * G::Co, q / HH, q % HH};
+        const int a = q / HH, b = q % HH;
+        const uint32_t mask = 1u | (b + 1 < G::OH ? 2u : 0u) | (a + 1 < G::OH ? 4u : 0u) |
+                              (a + 1 < G::OH && b + 1 < G::OH ? 8u : 0u);
+        return RowInfo{dy + ((n * G::OH + a) * G::OH + b) * G::Co, mask};
     }
-    __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& ri, int k) const {
-        const int nb = k / G::Co, co = k % G::Co;  // neighbour (da, db) = (nb >> 1, nb & 1)
-        const int oh = ri.a + (nb >> 1), ow = ri.b + (nb & 1);
-        if ((unsigned)oh >= (unsigned)G::OH || (unsigned)ow >= (unsigned)G::OH) return nullptr;
-        return dy + ri.base + (oh * G::OH + ow) * G::Co + co;
+    struct TapInfo {
+        int off, bit;
+    };
+    __device__ __forceinline__ TapInfo tap_info(int k) const {
+        const int nb = k / G::Co;  // neighbour (da, db) = (nb >> 1, nb & 1)
+        return k < K ? TapInfo{((nb >> 1) * G::OH + (nb & 1)) * G::Co + k % G::Co, nb} : TapInfo{0, 31};
+    }
+    __device__ __forceinline__ const float* a_ptr_tap(const RowInfo& r, const TapInfo& t) const {
+        return (r.vmask >> t.bit) & 1u ? r.ptr + t.off : nullptr;
     }
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     // epilogue column c (0..N-1) -> (class, ci); rows write 4 input pixels
@@ -594,6 +613,20 @@ struct Wgrad {
         if (row >= kOnesRow) return RowInfo{-1000, 0, 0};
         const int t = row / G::Ci;
         return RowInfo{t / 3 - 1, t % 3 - 1, row % G::Ci};
+    }
+    // per-chunk decode of a reduction index (sample, output pixel), then the row quad's pointer
+    struct RedInfo {
+        int base, ih, iw;
+    };
+    __device__ __forceinline__ RedInfo red_info(int m) const {
+        if (m >= kbeg + K) return RedInfo{0, -1000, -1000};
+        const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
+        return RedInfo{n * G::H * G::H * G::Ci, (pix / G::OH) * G::S, (pix % G::OH) * G::S};
+    }
+    __device__ __forceinline__ const float* a_ptr_red(const RowInfo& ri, const RedInfo& rd) const {
+        const int ih = rd.ih + ri.kh, iw = rd.iw + ri.kw;
+        if ((unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H) return nullptr;
+        return in + (rd.base + (ih * G::H + iw) * G::Ci + ri.ci);
     }
     // the 4 rows of `ri` at reduction index m (sample, output pixel)
     __device__ __forceinline__ const float* a_ptr_ri(const RowInfo& ri, int m) const {

@@ -175,51 +175,53 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
         // this thread's cp.async units: rows pt/8 + 32 j (j < 4), k-quad pt % 8; the rows' decode
         // (sample, window origin) is computed once per tile
         typename Op::RowInfo ri[4];
-        int ri_tile = -1;
-        auto a_issue = [&](int gg) {
+        // prefetch cursor (tile, chunk, ring slot), advanced incrementally: no divisions
+        int pf_tile = 0, pf_chunk = 0, pf_slot = 0;
+        auto a_issue = [&]() {
+            const int mm0 = (tile0 + pf_tile) * kBM, kk0 = op.kbeg + pf_chunk * kKC;
+            const uint32_t dst = araw + pf_slot * kARawTile;
+            // each warp copies exactly the part of the tile it reads back (rows 32q.., k half h),
+            // so only a warp-level sync separates copy and read
             if constexpr (Op::AM == 0) {
-                const int ti = gg / nchunks;
-                const int mm0 = (tile0 + ti) * kBM, kk0 = op.kbeg + (gg % nchunks) * kKC;
-                if (ti != ri_tile) {
+                // unit j: row 32q + lane/4 + 8j, k-quad 4h + lane%4 (4 lanes = one row's 64 bytes)
+                if (pf_chunk == 0) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) ri[j] = op.row_info(mm0 + (pt >> 3) + 32 * j);
-                    ri_tile = ti;
+                    for (int j = 0; j < 4; ++j) ri[j] = op.row_info(mm0 + q * 32 + (lane >> 2) + 8 * j);
                 }
-                const uint32_t dst = araw + (gg % kARaw) * kARawTile;
-                const int kq = pt & 7, k = kk0 + kq * 4;
+                const int kq = h * 4 + (lane & 3);
+                const auto tap = op.tap_info(kk0 + kq * 4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int r = (pt >> 3) + 32 * j;
-                    const float* src = op.a_ptr_ri(ri[j], k);
+                    const int r = q * 32 + (lane >> 2) + 8 * j;
+                    const float* src = op.a_ptr_tap(ri[j], tap);
                     cp16(dst + (r * kRawLdK + kq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
                 }
             } else {
-                // MN-contiguous A: unit (row quad pt % 32, reduction k = pt / 32 + 8 j): 16 bytes =
-                // 4 consecutive rows at one k; a warp covers 512 contiguous bytes
-                const int ti = gg / nchunks;
-                const int mm0 = (tile0 + ti) * kBM, kk0 = op.kbeg + (gg % nchunks) * kKC;
-                const int rq = pt & 31;
-                if (ti != ri_tile) {
-                    ri[0] = op.row_info(mm0 + rq * 4);
-                    ri_tile = ti;
-                }
-                const uint32_t dst = araw + (gg % kARaw) * kARawTile;
+                // MN-contiguous A: unit j = (row quad 8q + lane%8, k = 16h + lane/8 + 4j): 16 bytes =
+                // 4 consecutive rows at one k
+                const int rq = q * 8 + (lane & 7);
+                if (pf_chunk == 0) ri[0] = op.row_info(mm0 + rq * 4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int k = (pt >> 5) + 8 * j;
-                    const float* src = op.a_ptr_ri(ri[0], kk0 + k);
+                    const int k = h * 16 + (lane >> 3) + 4 * j;
+                    const float* src = op.a_ptr_red(ri[0], op.red_info(kk0 + k));
                     cp16(dst + (k * kRawLdMN + rq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
                 }
             }
             asm volatile("cp.async.commit_group;");
+            if (++pf_chunk == nchunks) {
+                pf_chunk = 0;
+                ++pf_tile;
+            }
+            if (++pf_slot == kARaw) pf_slot = 0;
         };
         for (int gg = 0; gg < kPre; ++gg) {
             if (gg < total)
-                a_issue(gg);
+                a_issue();
             else
                 asm volatile("cp.async.commit_group;");
         }
-        int g = 0;
+        int g = 0, rd_slot = 0;
         float4 bn[4];  // next chunk's B registers (non-image Ops)
         for (int i = 0; i < ntiles; ++i) {
             const int m0 = (tile0 + i) * kBM;
@@ -259,9 +261,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                 }
                 float a[16];
                 asm volatile("cp.async.wait_group %0;" ::"n"(kPre - 1) : "memory");  // own copies of chunk g landed
-                producers_sync();  // everyone's copies landed; chunk g-1's buffer is consumed
-                if (g + kPre < total) a_issue(g + kPre); else asm volatile("cp.async.commit_group;");
-                const char* rawg = smem + Plan::ARawOff + (g % kARaw) * kARawTile;
+                __syncwarp();  // the warp's copies landed; its reads of chunk g-1's slot are done
+                if (g + kPre < total) a_issue(); else asm volatile("cp.async.commit_group;");
+                const char* rawg = smem + Plan::ARawOff + rd_slot * kARawTile;
+                if (++rd_slot == kARaw) rd_slot = 0;
                 if constexpr (Op::AM == 0) {
                     const float4* rp = reinterpret_cast<const float4*>(rawg + ((q * 32 + lane) * kRawLdK + h * 16) * 4);
 #pragma unroll
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                     }
                 }
                 // A hi/lo -> TMEM
+#ifndef SMX_DBG_NO_ASTORE
                 {
                     float lo[16];
 #pragma unroll
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                     tmem_st16(ta, a);
                     if (!Op::A_EXACT) tmem_st16(ta + 32, lo);
                 }
+#endif
                 // B hi/lo -> smem canonical
                 if constexpr (Op::B_IMAGE) {
                 } else if constexpr (Op::BMODE == 0) {
@@ -362,7 +367,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                     const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
                     const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
                     const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
+#ifdef SMX_DBG_NO_MMA
+                    for (int st = 0; st < 0; ++st) {
+#else
                     for (int st = 0; st < ksteps; ++st) {
+#endif
                         const uint32_t o = st * 2 * lbo;
                         const uint64_t dbh = smem_desc(bhi + o, lbo, 128), dbl = smem_desc(blo + o, lbo, 128);
                         uint32_t accum = (unit_start && st == 0) ? 0u : 1u;

@@ -200,13 +200,13 @@ constexpr int conv_tpc() {
 template <>
 constexpr int conv_tpc<cnn::ctc::Fwd<1>>() { return 8; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 4; }
+constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 16; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 2; }
+constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 8; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 4; }
+constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 16; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 2; }
+constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 8; }
 
 template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {

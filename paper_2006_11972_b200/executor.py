@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libsmx.so"
+LIB_PATH = Path(os.environ["SMX_LIB_PATH"]) if os.environ.get("SMX_LIB_PATH") else _PKG / "libsmx.so"  # override: profiling variants
 
 SMX_OK, SMX_ECONFIG, SMX_EINTEGRITY, SMX_EDEVICE = 0, 1, 2, 3
 MODEL_MLP = 0
