@@ -5,12 +5,13 @@ A bench "step" is one complete study run through the engine (plan insert -> stag
 critical-path schedule -> grouped GPU training / SAVE / LOAD / EVAL -> metrics recorded), STAGE
 mode.  TES = sum over trials of their steps / seconds.
 
-Workload at N GPUs ("scaling": "weak"): N studies over the C3 search space
-(paper_2006_11972_b200/studies/c3_random.json: 256 random trials x 2000 steps, sampler seeds
-0..N-1) merged into one plan whose root subtrees are LPT-partitioned over the N ranks — no
-collective on the data path.  N = 1 is exactly C3.
+Workloads (`--workload`, default c2 = BASELINE.json configs[1]): c2 the CNN grid (64 trials x
+1200 steps, one replica study per rank, weak scaling); c3 N studies over the C3 space merged and
+root-partitioned over N ranks (weak); c4_sha / c4_asha tuned C4 studies (replicas); c5 four
+studies over one space merged and partitioned (strong).  No collective on the data path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--gemm exact|tc]
+                    [--workload c2|c3|c4_sha|c4_asha|c5] [--no-cpu] [--no-trial]
 
 Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §6).
 """
@@ -144,7 +145,11 @@ WORKLOADS = {
                                "one study per rank (replicas)", 128, 256),
     "c4_asha": ("c4_asha", True, "C4 ASHA (eta 4, rungs 150/600/1200 steps, 448-trial grid, 128 in flight), "
                                  "MLP 784-256-256-10, one study per rank (replicas)", 128, 256),
+    "c5": ("c5_space", False, "C5 multi-study merge: 4 studies (256 random trials x 2000 steps each, sampler seeds "
+                              "0..3) over one space, one plan (732 leaves, q = 1.868), MLP 784-256-256-10, root "
+                              "subtrees partitioned over {n} rank(s)", 128, 256),
 }
+STRONG = {"c5"}  # fixed total work (4 studies) split over the ranks
 DEFAULT_WORKLOAD = "c2"  # BASELINE.json configs[1]: the 1-GPU CNN grid search
 
 
@@ -160,7 +165,7 @@ def workload(name: str, n_studies: int):
     if base.get("sampler", {}).get("kind") != "random":  # grid: identical replica per rank
         return [json.dumps(base)], False, desc
     specs = []
-    for s in range(n_studies):
+    for s in range(4 if name in STRONG else n_studies):
         sp = dict(base)
         sp["sampler"] = {**base["sampler"], "seed": s}
         specs.append(json.dumps(sp))
@@ -282,7 +287,8 @@ def main():
     gemm_mode = ex.GEMM_TC if args.gemm == "tc" else ex.GEMM_EXACT
     # random-sampled studies differ per rank and are merged + root-partitioned; tuned studies and
     # grids run one replica per rank
-    part = {"rank": rank, "world": world} if (not tuned and len(specs) == world and world > 1) else {}
+    partitioned = not tuned and world > 1 and (len(specs) == world or args.workload in STRONG)
+    part = {"rank": rank, "world": world} if partitioned else {}
     cnn = info["key"]["model"] == "cnn"
     max_batch = WORKLOADS[args.workload][4]
     eng = host.Engine.for_study(specs[0], devices=[local], slots_per_gpu=args.slots, ckpts_per_gpu=1024,
@@ -437,7 +443,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if args.workload in STRONG else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "config": {"workload": desc,
                        "gemm": args.gemm, "slots_per_gpu": args.slots, "trials": len(info["trials"]) * len(specs),
                        "trial_steps": trial_steps, "unique_stage_steps": stage_steps,

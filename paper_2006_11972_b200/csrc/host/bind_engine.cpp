@@ -186,6 +186,23 @@ void bind_engine(py::module_& m) {
         });
     });
 
+    // merge rate p (one study) or q (several, SPEC.md analysis kwise_merge_rate) over one plan
+    m.def("merge_rate_specs", [](const std::vector<std::string>& specs) {
+        return translate([&] {
+            std::vector<TrialConfig> all;
+            CompatKey key;
+            for (std::size_t i = 0; i < specs.size(); ++i) {
+                const StudySpec s = parse_study(specs[i]);
+                if (i == 0)
+                    key = s.key;
+                else if (!(s.key == key))
+                    throw ConfigError("merge-rate: studies have different compatibility keys");
+                all.insert(all.end(), s.trials.begin(), s.trials.end());
+            }
+            return merge_rate(key, all);
+        });
+    });
+
     m.def("expand_study", [](const std::string& spec_json) {
         return translate([&] {
             const StudySpec s = parse_study(spec_json);
