@@ -48,7 +48,8 @@ struct WsPlan {
     static constexpr int N = Op::kMaxN;
     static constexpr int Stages = N >= 128 ? 3 : kMaxStages;
     static constexpr int BStage = N * 256;                          // hi + lo tiles
-    static constexpr int Sacc = Op::kSegChunks > 0 ? kBM * N * 4 : 0;
+    static constexpr int SaccLd = N + 4;                            // floats per row (conflict-free)
+    static constexpr int Sacc = kBM * SaccLd * 4;                   // tile sums [row][N + 4]
     static constexpr int Fixed = Stages * BStage + 128 + Sacc;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
     static constexpr int ARaw = ARawMax > 8 ? 8 : ARawMax;
@@ -194,6 +195,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                 for (int j = 0; j < 4; ++j) {
                     const int r = q * 32 + (lane >> 2) + 8 * j;
                     const float* src = op.a_ptr_tap(ri[j], tap);
+#ifdef SMX_DBG_NO_LOAD
+                    src = nullptr;
+#endif
                     cp16(dst + (r * kRawLdK + kq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
                 }
             } else {
@@ -397,97 +401,100 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
     } else {
         // ================= epilogue =================
         const int q = warp & 3;
-        float4* sacc = reinterpret_cast<float4*>(smem + Plan::SaccOff);  // [col/4][row], segmented Ops only
+        static_assert(Op::kSegChunks > 0, "the epilogue stages every tile in shared memory");
+        float* sacc = reinterpret_cast<float*>(smem + Plan::SaccOff);  // [row][N + 4]
+        constexpr int LD = Plan::SaccLd;
         const int row = q * 32 + lane;
+        const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
-            const int m = (tile0 + i) * kBM + row;
-            const bool live = m < M;
-            if (Op::kSegChunks > 0) {
-                // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
-                for (int j = 0; j < nseg; ++j, ++un) {
-                    const int acc_i = un & 1, use = un >> 1;
-                    mbar_wait(&accf[acc_i], use & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    for (int c0 = 0; c0 < nt; c0 += 16) {
-                        uint32_t r[16];
-                        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;");
-                        if (c0 + 16 >= nt) {
-                            asm volatile("tcgen05.fence::before_thread_sync;");
-                            mbar_arrive(&acce[acc_i]);
-                        }
-#pragma unroll
-                        for (int jj = 0; jj < 16; jj += 4) {
-                            float4* sp = sacc + ((c0 + jj) >> 2) * kBM + row;
-                            const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
-                                                          __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
-                            if (j == 0) {
-                                *sp = nv;
-                            } else {
-                                float4 o = *sp;
-                                o.x = __fadd_rn(o.x, nv.x);
-                                o.y = __fadd_rn(o.y, nv.y);
-                                o.z = __fadd_rn(o.z, nv.z);
-                                o.w = __fadd_rn(o.w, nv.w);
-                                *sp = o;
-                            }
-                        }
-                    }
-                }
-            }
-            int acc_i = 0;
-            if (Op::kSegChunks == 0) {
-                acc_i = un & 1;
-                const int use = un >> 1;
-                ++un;
+            const int mt0 = (tile0 + i) * kBM;
+            // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
+            for (int j = 0; j < nseg; ++j, ++un) {
+                const int acc_i = un & 1, use = un >> 1;
                 mbar_wait(&accf[acc_i], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-            }
-            for (int c0 = 0; c0 < nt; c0 += 16) {
-                uint32_t r[16];
-                if (Op::kSegChunks > 0) {
-#pragma unroll
-                    for (int jj = 0; jj < 16; jj += 4) {
-                        const float4 t = sacc[((c0 + jj) >> 2) * kBM + row];
-                        r[jj] = __float_as_uint(t.x); r[jj + 1] = __float_as_uint(t.y);
-                        r[jj + 2] = __float_as_uint(t.z); r[jj + 3] = __float_as_uint(t.w);
-                    }
-                } else {
+                for (int c0 = 0; c0 < nt; c0 += 16) {
+                    uint32_t r[16];
                     tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;");
                     if (c0 + 16 >= nt) {
                         asm volatile("tcgen05.fence::before_thread_sync;");
-                        mbar_arrive(&acce[acc_i]);  // accumulator free for unit un + 1
+                        mbar_arrive(&acce[acc_i]);
                     }
-                }
-                if (!live) continue;
 #pragma unroll
-                for (int j0 = 0; j0 < 16; j0 += 4) {
-                    const int n0 = c0 + j0;
-                    if (n0 >= N) continue;
-                    float x[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[j0 + j]);
-                    if constexpr (Op::EPI == ctc::kEpiBiasRelu) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const float t = __fadd_rn(x[j], __ldg(op.bias + n0 + j));
-                            x[j] = t > 0.0f ? t : 0.0f;
+                    for (int jj = 0; jj < 16; jj += 4) {
+                        float4* sp = reinterpret_cast<float4*>(sacc + row * LD + c0 + jj);
+                        const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
+                                                      __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
+                        if (j == 0) {
+                            *sp = nv;
+                        } else {
+                            float4 o = *sp;
+                            o.x = __fadd_rn(o.x, nv.x);
+                            o.y = __fadd_rn(o.y, nv.y);
+                            o.z = __fadd_rn(o.z, nv.z);
+                            o.w = __fadd_rn(o.w, nv.w);
+                            *sp = o;
                         }
-                        *reinterpret_cast<float4*>(op.c_at(m, n0)) = make_float4(x[0], x[1], x[2], x[3]);
-                    } else if constexpr (Op::EPI == ctc::kEpiMask) {
-                        const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_at(m, n0)));
-                        *reinterpret_cast<float4*>(op.c_at(m, n0)) =
-                            make_float4(mk.x > 0.0f ? x[0] : 0.0f, mk.y > 0.0f ? x[1] : 0.0f,
-                                        mk.z > 0.0f ? x[2] : 0.0f, mk.w > 0.0f ? x[3] : 0.0f);
-                    } else {
-                        float* ptp = op.part + (long long)op.split * N * Op::kPartLd + m;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) ptp[(long long)(n0 + j) * Op::kPartLd] = x[j];
                     }
                 }
             }
+#ifndef SMX_DBG_NO_EPI
+            if constexpr (Op::EPI == ctc::kEpiBiasRelu) {
+                // the output tile is one contiguous block (rows = consecutive pixels): cooperative,
+                // coalesced write-out, consecutive threads = consecutive 16 bytes
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // the whole tile is in sacc
+                const int q4 = N / 4;
+                for (int e = et; e < kBM * q4; e += 128) {
+                    const int r = e / q4, c4 = e % q4, m = mt0 + r;
+                    if (m >= M) continue;
+                    float4 x = *reinterpret_cast<const float4*>(sacc + r * LD + 4 * c4);
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(op.bias + 4 * c4));
+                    x.x = __fadd_rn(x.x, b.x); x.y = __fadd_rn(x.y, b.y);
+                    x.z = __fadd_rn(x.z, b.z); x.w = __fadd_rn(x.w, b.w);
+                    *reinterpret_cast<float4*>(op.c_at(m, 4 * c4)) =
+                        make_float4(x.x > 0.0f ? x.x : 0.0f, x.y > 0.0f ? x.y : 0.0f, x.z > 0.0f ? x.z : 0.0f,
+                                    x.w > 0.0f ? x.w : 0.0f);
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile
+            } else if constexpr (Op::EPI == ctc::kEpiPartT) {
+                // transposed partials: lanes = consecutive rows of one column (coalesced)
+                const int m = mt0 + row;
+                if (m < M) {
+                    float* pt = op.part + (long long)op.split * N * Op::kPartLd + m;
+                    for (int col = 0; col < N; ++col) pt[(long long)col * Op::kPartLd] = sacc[row * LD + col];
+                }
+            } else {
+                // ReLU-masked scatter to the 4 sub-pixels, cooperative: thread = fixed float4 column
+                // (class, 4 channels), rows r0, r0 + 4, ...; a warp covers one row's N columns =
+                // whole 128-byte pixel segments.  Mask loads are issued 8 rows ahead of their use.
+                constexpr int Q4 = Plan::N / 4, RSTEP = 128 / Q4, PER = kBM / RSTEP, U = 8;
+                static_assert(128 % Q4 == 0 && PER % U == 0, "epilogue mapping");
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // the whole tile is in sacc
+                const int c4 = et % Q4, r0 = et / Q4;
+                for (int i0 = 0; i0 < PER; i0 += U) {
+                    float4 mk[U];
+                    long long off[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int m = mt0 + r0 + RSTEP * (i0 + u);
+                        off[u] = m < M ? op.pix_off(m, 4 * c4) : -1;
+                        mk[u] = off[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(op.act + off[u]))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (off[u] < 0) continue;
+                        const float4 x = *reinterpret_cast<const float4*>(sacc + (r0 + RSTEP * (i0 + u)) * LD + 4 * c4);
+                        *reinterpret_cast<float4*>(op.dx + off[u]) =
+                            make_float4(mk[u].x > 0.0f ? x.x : 0.0f, mk[u].y > 0.0f ? x.y : 0.0f,
+                                        mk[u].z > 0.0f ? x.z : 0.0f, mk[u].w > 0.0f ? x.w : 0.0f);
+                    }
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile
+            }
+#endif
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
