@@ -37,7 +37,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 # (profiles/<round>/), keyed by kernel; filled in after each capture.
 TRAFFIC: dict = {
     # profiles/r01/ncu_conv2_fwd_full.txt: 64 groups at bs 128 (= the bench's roofline launch)
-    "conv_ws_kernel<Fwd<2>>": 1_083_470_000 + 504_293_120,
+    "conv_ws_kernel<Fwd<2>>": 1_083_516_000 + 506_999_552,
 }
 METRIC = "trial-equivalent train steps/sec per study"
 UNIT = "trial-steps/s"

@@ -217,8 +217,11 @@ void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) 
            "conv smem attribute");
         configured = true;
     }
-    constexpr int tpc = conv_tpc<Op>();
+    // tiles per CTA: as many as the Op likes (fewer pipeline fills) while the grid still gives
+    // every SM at least two CTAs; it changes only the work split, never the arithmetic
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
+    int tpc = conv_tpc<Op>();
+    while (tpc > 1 && (long long)gx * ((mtiles + tpc - 1) / tpc) * groups < 2 * 148) tpc /= 2;
     dim3 grid(gx, (mtiles + tpc - 1) / tpc, groups);
     cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::kWsThreads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, tpc);
     launch_check(c, "conv_ws");
