@@ -432,7 +432,7 @@ def main():
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
         roofline = dict(kernels["K1_fwd1_gemm"])
-        roofline["kernel"] = "gemm_tc_ts_kernel<0,0,BiasRelu> (layer-1 forward, 64 groups x 128x256x784)"
+        roofline["kernel"] = "conv_ws_kernel<DenseOp<0,0,BiasRelu,exact A>> (MLP layer-1 forward, 64 groups x 128x256x784)"
     roofline["traffic"] = TRAFFIC.get(roofline["kernel"].split(" ")[0])
 
     cpu = None

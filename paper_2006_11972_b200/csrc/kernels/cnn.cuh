@@ -4,11 +4,12 @@
 //
 // Layout (HBM): images NHWC 32x32x4 (channel 3 == 0), activations NHWC per slot, conv weights
 // [Cout][kh*3+kw][Cin_pad].  Exact mode runs the SIMT kernels below (one thread per output, the
-// fmaf chain order of oracle/cnn.c); tensor-core mode runs every conv as an implicit GEMM on
-// tcgen05 (conv_tc_kernel): forward M = pixels, K = (tap, cin); input gradient per stride-2
-// parity class (dense taps only); weight gradient with the reduction over (sample, pixel) split
-// into fixed 2048-row ranges reduced in order by wgrad_reduce_kernel (deterministic, grouping
-// invariant) and the bias gradient as an extra all-ones row of the im2col operand.
+// fmaf chain order of oracle/cnn.c); tensor-core mode runs conv2/conv3 as implicit GEMMs on
+// tcgen05 through the Op policies below and the warp-specialised kernel of conv_ws.cuh: forward
+// M = pixels, K = (tap, cin); input gradient as one sub-pixel GEMM; weight gradient with the
+// reduction over (sample, pixel) split into fixed 2048-row ranges reduced in order by
+// wgrad_reduce_kernel (deterministic, grouping invariant) and the bias gradient as an extra
+// all-ones row of the im2col operand.  conv1 (K = 27) uses fp32 SIMT kernels in both modes.
 #pragma once
 
 #include "common.cuh"
@@ -438,26 +439,14 @@ __global__ void __launch_bounds__(128) head_dg_kernel(ConvArgs p) {
     for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = a3[pix * kFeat + c] > 0.0f ? dg : 0.0f;
 }
 
-// ---- tensor-core mode: implicit-GEMM convolutions on tcgen05 ------------------------------
-// The core is the TS variant of gemm_tc.cuh (A: cp.async raw -> registers -> hi/lo split ->
-// TMEM; B: cp.async raw -> smem hi/lo split -> UMMA canonical layout; 3xTF32, one thread issues
-// the MMAs, mbarrier-released double buffers), with the operands gathered by implicit-GEMM
-// address functions instead of a leading dimension, and several M tiles per CTA processed as one
-// flattened chunk stream (the next tile's loads overlap the current tile's epilogue).
+// ---- tensor-core mode: implicit-GEMM Op policies for conv_ws.cuh ---------------------------
+// Each Op describes one GEMM-shaped conv pass: its per-group setup, the implicit-GEMM address
+// functions of the A operand (row decode once per tile, tap decode once per K chunk), the B
+// operand (pre-split weight image or register gather) and the epilogue target.
 namespace ctc {
 using namespace smx::tc3;
 
-enum { kEpiBiasRelu = 0, kEpiMask = 1, kEpiPartT = 2 };
-constexpr int kConvSmem = kSmem + 512;  // + the tile's bias slice
-// TMEM: two accumulator regions (columns [0,128) and [128,256)) used for alternating segments
-// of kSeg chunks, then the A operand hi/lo double buffer at 256 + 64 b.  Each finished segment is
-// added into fp32 registers with round-to-nearest adds: the tensor core's own fp32 accumulation
-// is not round-to-nearest, and over long reductions (the weight gradients sum up to 2048 rows
-// per split) its error grows linearly; promoting every kSeg * 32 = 64 products keeps the result
-// at fp32 accuracy.
-constexpr int kSeg = 2;
-constexpr int kConvTmemCols = 512;
-constexpr int kAOff = 256;
+enum { kEpiBiasRelu = 0, kEpiMask = 1, kEpiPartT = 2, kEpiBias = 3, kEpiStore = 4 };
 
 // source of zero-filled 16-byte copies (cp.async reads 0 bytes from it)
 __device__ __align__(16) float kZero16[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -479,7 +468,13 @@ struct Fwd {
         const float* ptr;  // input element (top-left of the 3x3 window, channel 0); may be out of range
         uint32_t vmask;    // bit t: tap t of the window lies inside the image (0 for rows >= M)
     };
-    __device__ void setup(const ConvArgs& p, const SlotView& v, int tile_y) {
+    using Args = ConvArgs;
+    __device__ __forceinline__ float4 bias4(int col) const { return __ldg(reinterpret_cast<const float4*>(bias + col)); }
+    __device__ __forceinline__ void store4(int m, int col, float4 x) const {
+        *reinterpret_cast<float4*>(out + (long long)m * G::Co + col) = x;
+    }
+    __device__ void setup(const ConvArgs& p, int z, int tile_y) {
+        const SlotView v = slot_view(p, p.slots[z]);
         img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
         in = layer_in<L>(p, v);
         w = v.w + G::OffW;
@@ -555,7 +550,9 @@ struct Dgrad {
         const float* ptr;  // dy at output pixel (a, b), channel 0
         uint32_t vmask;    // bit 2 da + db: neighbour (a + da, b + db) exists (0 for rows >= M)
     };
-    __device__ void setup(const ConvArgs& p, const SlotView& v, int half) {
+    using Args = ConvArgs;
+    __device__ void setup(const ConvArgs& p, int z, int half) {
+        const SlotView v = slot_view(p, p.slots[z]);
         dy = layer_dout<L>(p, v);
         w = v.w + G::OffW;
         act = layer_out<L - 1>(p, v);
@@ -596,6 +593,14 @@ struct Dgrad {
     }
     __device__ __forceinline__ float* c_at(int r, int col) const { return dx + pix_off(r, col); }
     __device__ __forceinline__ const float* mask_at(int r, int col) const { return act + pix_off(r, col); }
+    // masked epilogue: mask and output share the offset (input pixel, channel)
+    __device__ __forceinline__ long long mask_off(int r, int col) const { return pix_off(r, col); }
+    __device__ __forceinline__ float4 mask4(long long off) const {
+        return __ldg(reinterpret_cast<const float4*>(act + off));
+    }
+    __device__ __forceinline__ void store_masked(int, int, long long off, float4 x) const {
+        *reinterpret_cast<float4*>(dx + off) = x;
+    }
 };
 
 // Weight gradient, split s of the reduction: part[s][co][k] = sum_{m in split} im2col(in)[m][k] dy[m][co]
@@ -641,7 +646,12 @@ struct Wgrad {
     const float* dy;
     float* part;
     int M, N, K, kbeg, m0, split;
-    __device__ void setup(const ConvArgs& p, const SlotView& v, int s) {
+    using Args = ConvArgs;
+    __device__ __forceinline__ float* ct_at(int col, int m) const {
+        return part + ((long long)split * N + col) * kPartLd + m;
+    }
+    __device__ void setup(const ConvArgs& p, int z, int s) {
+        const SlotView v = slot_view(p, p.slots[z]);
         in = layer_in<L>(p, v);
         dy = layer_dout<L>(p, v);
         part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3);
@@ -666,215 +676,6 @@ struct Wgrad {
     __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
     __device__ __forceinline__ const float* mask_at(int, int) const { return nullptr; }
 };
-
-// cp.async of one operand tile through an address functor (16-byte units, zero fill).
-// MN == 0: unit (row, k-quad) -> f(row, k) points at 4 consecutive k of `row`;
-// MN == 1: unit (row-quad, k) -> f(row, k) points at rows row..row+3 at reduction index k.
-template <int MN, class F>
-__device__ __forceinline__ void load_tile(const F& f, int r0, int rows, int rlim, int k0, int klim, uint32_t raw) {
-    if (MN == 0) {
-        for (int u = threadIdx.x; u < rows * kKQ; u += kThreads) {
-            const int r = u / kKQ, kq = u % kKQ;
-            const int row = r0 + r, k = k0 + kq * 4;
-            const float* src = (row < rlim && k < klim) ? f(row, k) : nullptr;
-            cp16(raw + (r * kRawLdK + kq * 4) * 4, src ? src : kZero16, src ? 16 : 0);
-        }
-    } else {
-        for (int u = threadIdx.x; u < 32 * kKC; u += kThreads) {
-            const int rq = u & 31, k = u >> 5;
-            if (rq * 4 >= rows) continue;
-            const int row = r0 + rq * 4, kk = k0 + k;
-            const float* src = (row < rlim && kk < klim) ? f(row, kk) : nullptr;
-            cp16(raw + (k * kRawLdMN + rq * 4) * 4, src ? src : kZero16, src ? 16 : 0);
-        }
-    }
-}
-
-// grid: (x = class / split index, y = tile group, z = group); each CTA runs `tiles` M tiles.
-template <class Op>
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs p, int tiles) {
-    extern __shared__ __align__(1024) char smem[];
-    char* raw = smem;
-    char* hl = smem + 4 * kRawTile;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4 * kRawTile + 4 * kTile);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 4 * kRawTile + 4 * kTile + 32);
-    float* bias_s = reinterpret_cast<float*>(smem + 4 * kRawTile + 4 * kTile + 64);  // 128 floats
-
-    const SlotView v = slot_view(p, p.slots[blockIdx.z]);
-    Op op;
-    op.setup(p, v, blockIdx.x);
-    const int M = op.M, N = op.N, K = op.K;
-    const int tile0 = blockIdx.y * tiles;
-    const int ntiles = min(tiles, (M + kBM - 1) / kBM - tile0);
-    if (ntiles <= 0 || K <= 0) return;
-    const int nt = (N + 15) / 16 * 16;
-    const int nchunks = (K + kKC - 1) / kKC;
-    const int total = ntiles * nchunks;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int quad = warp & 3, kpart = warp >> 2;
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kConvTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;");
-    }
-    if constexpr (Op::EPI == kEpiBiasRelu)
-        for (int j = threadIdx.x; j < nt; j += kThreads) bias_s[j] = j < N ? op.bias[j] : 0.0f;
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t idesc = idesc_tf32(nt);
-    const uint32_t raw_u32 = smem_u32(raw), hl_u32 = smem_u32(hl);
-    const int klim = op.kbeg + K;
-
-    auto fa = [&](int r, int k) { return op.a_ptr(r, k); };
-    auto fb = [&](int r, int k) { return op.b_ptr(r, k); };
-    auto issue = [&](int g) {
-        const int b = g & 1;
-        const int m0 = (tile0 + g / nchunks) * kBM, k0 = op.kbeg + (g % nchunks) * kKC;
-        const int arlim = Op::kOnesRow >= 0 ? Op::kOnesRow : M;
-        load_tile<Op::AM>(fa, m0, kBM, arlim, k0, klim, raw_u32 + b * 2 * kRawTile);
-        load_tile<Op::BMODE>(fb, 0, nt, N, k0, klim, raw_u32 + b * 2 * kRawTile + kRawTile);
-    };
-    issue(0);
-    asm volatile("cp.async.commit_group;");
-    if (total > 1) issue(1);
-    asm volatile("cp.async.commit_group;");
-    float a_cur[kAK];
-    const int cols = nt / kParts;  // accumulator columns owned by this thread: [kpart*cols, +cols)
-    float racc[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) racc[j] = 0.0f;
-    // add accumulator region `reg` into racc (round-to-nearest fp32 adds)
-    auto drain = [&](int reg) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-            if (j < cols) {
-                uint32_t r[4];
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(reg * 128 + kpart * cols + j);
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                             : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-                for (int q = 0; q < 4; ++q) racc[j + q] = __fadd_rn(racc[j + q], __uint_as_float(r[q]));
-            }
-        }
-    };
-
-#pragma unroll 1
-    for (int g = 0; g < total; ++g) {
-        const int b = g & 1;
-        const int c = g % nchunks;
-        const int m0 = (tile0 + g / nchunks) * kBM;
-        const int k0 = op.kbeg + c * kKC;
-        asm volatile("cp.async.wait_group 1;");
-        if (g >= 2) mbar_wait(&bars[b], ((g - 2) >> 1) & 1);
-        __syncthreads();
-        read_a<Op::AM>(raw + b * 2 * kRawTile, quad * 32 + lane, kpart * kAK, a_cur);
-        if (Op::kOnesRow >= 0 && m0 + quad * 32 + lane == Op::kOnesRow) {
-#pragma unroll
-            for (int i = 0; i < kAK; ++i) a_cur[i] = (k0 + kpart * kAK + i < klim) ? 1.0f : 0.0f;
-        }
-        {
-            float hi[kAK], lo[kAK];
-#pragma unroll
-            for (int i = 0; i < kAK; ++i) {
-                hi[i] = Op::A_EXACT ? a_cur[i] : tf32_rna(a_cur[i]);
-                lo[i] = tf32_rna(__fsub_rn(a_cur[i], hi[i]));
-            }
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + kAOff + b * 64 + kpart * kAK;
-            tmem_st8(ta, hi);
-            if (!Op::A_EXACT) tmem_st8(ta + 32, lo);
-            asm volatile("tcgen05.wait::st.sync.aligned;");
-        }
-        {
-            char* h = hl + b * 2 * kTile;
-            split_b<Op::BMODE, Op::B_EXACT>(raw + b * 2 * kRawTile + kRawTile, nt, h, h + kTile);
-        }
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        if (g + 2 < total) issue(g + 2);
-        asm volatile("cp.async.commit_group;");
-        if (threadIdx.x == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t bhi = hl_u32 + b * 2 * kTile, blo = bhi + kTile;
-            const uint32_t ahi = tmem + kAOff + b * 64, alo = ahi + 32;
-            const uint32_t dacc = tmem + (uint32_t)(((c / kSeg) & 1) * 128);
-            const int ksteps = (min(kKC, klim - k0) + 7) / 8;
-#pragma unroll 1
-            for (int s = 0; s < ksteps; ++s) {
-                const uint32_t o = s * 2 * kLbo;
-                const uint64_t dbh = smem_desc(bhi + o, kLbo, 128), dbl = smem_desc(blo + o, kLbo, 128);
-                uint32_t acc = (c % kSeg == 0 && s == 0) ? 0u : 1u;
-                if (!Op::A_EXACT) {
-                    mma_ts(dacc, alo + s * 8, dbh, idesc, acc);
-                    acc = 1u;
-                }
-                if (!Op::B_EXACT) {
-                    mma_ts(dacc, ahi + s * 8, dbl, idesc, acc);
-                    acc = 1u;
-                }
-                mma_ts(dacc, ahi + s * 8, dbh, idesc, acc);
-            }
-            mma_commit(&bars[b]);
-        }
-        if (c > 0 && c % kSeg == 0) {
-            // the previous segment (other accumulator region) is complete once chunk g-1's MMAs are
-            mbar_wait(&bars[(g - 1) & 1], ((g - 1) >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            drain(((c - 1) / kSeg) & 1);
-        }
-        if (c != nchunks - 1) {
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            continue;
-        }
-
-        // ---- epilogue of this tile (the next tile's loads are already in flight)
-        mbar_wait(&bars[b], (g >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        drain((c / kSeg) & 1);
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        const int m = m0 + quad * 32 + lane;
-#pragma unroll
-        for (int jj = 0; jj < 32; jj += 4) {
-            const int c0 = kpart * cols + jj;
-            if (jj >= cols || m >= M || c0 >= N) continue;
-            float x[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) x[j] = racc[jj + j];
-            if constexpr (Op::EPI == kEpiBiasRelu) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float t = __fadd_rn(x[j], bias_s[c0 + j]);
-                    x[j] = t > 0.0f ? t : 0.0f;
-                }
-                *reinterpret_cast<float4*>(op.c_row(m) + c0) = make_float4(x[0], x[1], x[2], x[3]);
-            } else if constexpr (Op::EPI == kEpiMask) {
-                const float4 mk = __ldg(reinterpret_cast<const float4*>(op.mask_row(m) + c0));
-                *reinterpret_cast<float4*>(op.c_row(m) + c0) =
-                    make_float4(mk.x > 0.0f ? x[0] : 0.0f, mk.y > 0.0f ? x[1] : 0.0f, mk.z > 0.0f ? x[2] : 0.0f,
-                                mk.w > 0.0f ? x[3] : 0.0f);
-            } else {
-                float* pt = op.part + (long long)op.split * N * Op::kPartLd + m;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) pt[(long long)(c0 + j) * Op::kPartLd] = x[j];
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) racc[j] = 0.0f;
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kConvTmemCols));
-}
 
 }  // namespace ctc
 

@@ -118,7 +118,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ float lo_of(float a) { return __fsub_rn(a, __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
 
 template <class Op>
-__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int tiles) {
+__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Args p, int tiles) {
     extern __shared__ __align__(1024) char smem[];
     using Plan = WsPlan<Op>;
     constexpr int kBStage = Plan::BStage, kARaw = Plan::ARaw, kPre = Plan::ARaw - 1;  // prefetch distance
@@ -129,9 +129,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
     uint64_t* acce = accf + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
 
-    const SlotView v = slot_view(p, p.slots[blockIdx.z]);
     Op op;
-    op.setup(p, v, blockIdx.x);
+    op.setup(p, blockIdx.z, blockIdx.x);
     const int M = op.M, N = op.N, K = op.K;
     const int tile0 = blockIdx.y * tiles;
     const int ntiles = min(tiles, (M + kBM - 1) / kBM - tile0);
@@ -441,30 +440,32 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
                 }
             }
 #ifndef SMX_DBG_NO_EPI
-            if constexpr (Op::EPI == ctc::kEpiBiasRelu) {
-                // the output tile is one contiguous block (rows = consecutive pixels): cooperative,
-                // coalesced write-out, consecutive threads = consecutive 16 bytes
+            if constexpr (Op::EPI == ctc::kEpiBiasRelu || Op::EPI == ctc::kEpiBias || Op::EPI == ctc::kEpiStore) {
+                // row-major output tile: cooperative, coalesced write-out, consecutive threads =
+                // consecutive 16 bytes of a row
                 asm volatile("bar.sync 2, 128;" ::: "memory");  // the whole tile is in sacc
                 const int q4 = N / 4;
                 for (int e = et; e < kBM * q4; e += 128) {
                     const int r = e / q4, c4 = e % q4, m = mt0 + r;
                     if (m >= M) continue;
+                    if (4 * c4 >= N) continue;
                     float4 x = *reinterpret_cast<const float4*>(sacc + r * LD + 4 * c4);
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(op.bias + 4 * c4));
-                    x.x = __fadd_rn(x.x, b.x); x.y = __fadd_rn(x.y, b.y);
-                    x.z = __fadd_rn(x.z, b.z); x.w = __fadd_rn(x.w, b.w);
-                    *reinterpret_cast<float4*>(op.c_at(m, 4 * c4)) =
-                        make_float4(x.x > 0.0f ? x.x : 0.0f, x.y > 0.0f ? x.y : 0.0f, x.z > 0.0f ? x.z : 0.0f,
-                                    x.w > 0.0f ? x.w : 0.0f);
+                    if constexpr (Op::EPI != ctc::kEpiStore) {
+                        const float4 b = op.bias4(4 * c4);
+                        x.x = __fadd_rn(x.x, b.x); x.y = __fadd_rn(x.y, b.y);
+                        x.z = __fadd_rn(x.z, b.z); x.w = __fadd_rn(x.w, b.w);
+                    }
+                    if constexpr (Op::EPI == ctc::kEpiBiasRelu)
+                        x = make_float4(x.x > 0.0f ? x.x : 0.0f, x.y > 0.0f ? x.y : 0.0f, x.z > 0.0f ? x.z : 0.0f,
+                                        x.w > 0.0f ? x.w : 0.0f);
+                    op.store4(m, 4 * c4, x);
                 }
                 asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile
             } else if constexpr (Op::EPI == ctc::kEpiPartT) {
-                // transposed partials: lanes = consecutive rows of one column (coalesced)
+                // transposed outputs: lanes = consecutive rows of one column (coalesced)
                 const int m = mt0 + row;
-                if (m < M) {
-                    float* pt = op.part + (long long)op.split * N * Op::kPartLd + m;
-                    for (int col = 0; col < N; ++col) pt[(long long)col * Op::kPartLd] = sacc[row * LD + col];
-                }
+                if (m < M)
+                    for (int col = 0; col < N; ++col) *op.ct_at(col, m) = sacc[row * LD + col];
             } else {
                 // ReLU-masked scatter to the 4 sub-pixels, cooperative: thread = fixed float4 column
                 // (class, 4 channels), rows r0, r0 + 4, ...; a warp covers one row's N columns =
@@ -479,17 +480,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(ConvArgs p, int 
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int m = mt0 + r0 + RSTEP * (i0 + u);
-                        off[u] = m < M ? op.pix_off(m, 4 * c4) : -1;
-                        mk[u] = off[u] >= 0 ? __ldg(reinterpret_cast<const float4*>(op.act + off[u]))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                        off[u] = (m < M && 4 * c4 < N) ? op.mask_off(m, 4 * c4) : -1;
+                        mk[u] = off[u] >= 0 ? op.mask4(off[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (off[u] < 0) continue;
                         const float4 x = *reinterpret_cast<const float4*>(sacc + (r0 + RSTEP * (i0 + u)) * LD + 4 * c4);
-                        *reinterpret_cast<float4*>(op.dx + off[u]) =
+                        op.store_masked(mt0 + r0 + RSTEP * (i0 + u), 4 * c4, off[u],
                             make_float4(mk[u].x > 0.0f ? x.x : 0.0f, mk[u].y > 0.0f ? x.y : 0.0f,
-                                        mk[u].z > 0.0f ? x.z : 0.0f, mk[u].w > 0.0f ? x.w : 0.0f);
+                                        mk[u].z > 0.0f ? x.z : 0.0f, mk[u].w > 0.0f ? x.w : 0.0f));
                     }
                 }
                 asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile

@@ -24,6 +24,7 @@
 #include "kernels/step_kernels.cuh"
 #include "kernels/cnn.cuh"
 #include "kernels/conv_ws.cuh"
+#include "kernels/dense_ws.cuh"
 
 using namespace smx;
 
@@ -119,32 +120,37 @@ GemmArgs base_args(smx_ctx* c, const int* d_slots) {
     return a;
 }
 
-// Weight-gradient GEMMs (row-contiguous A: batch-major gradients) use the TS variant whose A
-// operand goes registers -> TMEM; the rest use the SS variant (both operands through smem).
-template <int AM, int BMODE, int EPI>
-void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
-    constexpr bool kTs = true;
-    static bool configured = false;  // per instantiation (device-independent attribute)
+// Tensor-core GEMMs of the MLP: the warp-specialised tcgen05 kernel (conv_ws.cuh) with the dense
+// Op policy (dense_ws.cuh); operands flagged as synthetic data are exact in tf32 and skip their
+// lo MMA.
+template <class Op>
+void dense_ws_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
+    static bool configured = false;
     if (!configured) {
-        if (kTs)
-            ck(cudaFuncSetAttribute(tc3::gemm_tc_ts_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc3::kSmem),
-               "tc smem attribute");
-        else
-            ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<AM, BMODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::kSmem),
-               "tc smem attribute");
+        ck(cudaFuncSetAttribute(cnn::ws::conv_ws_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cnn::ws::ws_smem<Op>()),
+           "dense smem attribute");
         configured = true;
     }
+    const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
+    dim3 grid((a.N + 127) / 128, mtiles, groups);
+    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::kWsThreads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, 1);
+    launch_check(c, "dense_ws");
+}
+
+template <int AM, int BMODE, int EPI>
+void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
     if ((a.a.ld & 3) || (a.b.ld & 3))
         fail(SMX_ECONFIG, "tensor-core GEMM needs 16-byte aligned operand rows (ld % 4 == 0)");
-    const int mt = (m_max + tc::kBM - 1) / tc::kBM;
-    dim3 grid((a.N + tc::kBN - 1) / tc::kBN, mt, groups);
-    if (kTs)
-        tc3::gemm_tc_ts_kernel<AM, BMODE, EPI><<<grid, tc3::kThreads, tc3::kSmem, c->cur>>>(a, tc3::kBN);
-    else
-        tc::gemm_tc_kernel<AM, BMODE, EPI><<<grid, tc::kThreads, tc::kSmem, c->cur>>>(a, tc::kBN);
-    launch_check(c, "gemm_tc");
+    constexpr int wepi = EPI == tc::kTcStore ? dws::kEpiStore : EPI == tc::kTcBiasRelu ? dws::kEpiBiasRelu
+                         : EPI == tc::kTcBias ? dws::kEpiBias : EPI == tc::kTcMask ? dws::kEpiMask : dws::kEpiPartT;
+    if constexpr (AM == 0 && BMODE == 0 && EPI == tc::kTcBiasRelu) {
+        if (a.a.from_data) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, true, false>>(c, a, groups, m_max);
+    }
+    if constexpr (AM == 1 && BMODE == 1 && EPI == tc::kTcStore) {
+        if (a.b.from_data) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, true>>(c, a, groups, m_max);
+    }
+    dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, false>>(c, a, groups, m_max);
 }
 
 template <int AM, int BMODE, int EPI>
