@@ -38,7 +38,8 @@ constexpr int kEpiWarp0 = 8;                     // warps 8-11
 constexpr int kMmaWarp = 12;
 constexpr int kWsThreads = 13 * 32;
 constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K-major canonical, N <= 128
-constexpr int kARawTile = kBM * kRawLdK * 4;     // raw A tile [128 rows][32 + 4 pad]
+constexpr int kARawTile = kBM * kKC * 4;         // raw A tile, 16 KB: [128 rows][32 k] (16-B units
+                                                 // XOR-swizzled by row) or [32 k][128 rows]
 
 // Shared-memory plan of one Op, sized by its N (the B tiles and the segment sums scale with it):
 // kStages B stages | kARaw raw A tiles | barriers | segment sums.  The raw-A ring takes what is
@@ -48,12 +49,13 @@ struct WsPlan {
     static constexpr int N = Op::kMaxN;
     static constexpr int Stages = N >= 128 ? 3 : kMaxStages;
     static constexpr int BStage = N * 256;                          // hi + lo tiles
-    static constexpr int SaccLd = N + 4;                            // floats per row (conflict-free)
-    static constexpr int Sacc = kBM * SaccLd * 4;                   // tile sums [row][N + 4]
+    static constexpr int Sacc = kBM * N * 4;                        // tile sums [row][N], 16-B units
+                                                                    // XOR-swizzled by row
     static constexpr int Fixed = Stages * BStage + 128 + Sacc;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
-    static constexpr int ARaw = ARawMax > 8 ? 8 : ARawMax;
-    static_assert(ARaw >= 3, "shared memory plan");
+    // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
+    static constexpr int ARaw = (ARawMax > 8 ? 8 : ARawMax) & ~1;
+    static_assert(ARaw >= 4, "shared memory plan");
     static constexpr int ARawOff = Stages * BStage;
     static constexpr int BarOff = ARawOff + ARaw * kARawTile;
     static constexpr int SaccOff = BarOff + 128;
@@ -97,7 +99,7 @@ __device__ __forceinline__ void split1(float a, float& h, float& l) {
     l = tf32_rna(__fsub_rn(a, h));
 }
 
-__device__ __forceinline__ void producers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], kProducers + (Op::B_IMAGE ? 1 : 0));
+            mbar_init(&full[s], 128 + (Op::B_IMAGE ? 1 : 0));  // one producer group (+ the bulk copy)
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -167,165 +169,176 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
 
     if (warp < kEpiWarp0) {
         // ================= producers =================
-        const int q = warp & 3, h = warp >> 2;  // TMEM lane quadrant, k half
-        const int pt = threadIdx.x;             // 0..255
+        // Two groups of four warps (one per TMEM lane quadrant) take alternate K chunks, so two
+        // chunks are in flight; within a group warp q owns rows 32q..32q+31 and all 32 k.
+        const int grp = warp >> 2, q = warp & 3;
+        const int gt = threadIdx.x & 127;  // thread within the group
+        constexpr int kDw = kARaw / 2 - 1; // own chunks prefetched ahead
         const uint32_t araw = smem_u32(smem + Plan::ARawOff);
-        // K-contiguous A: coalesced cp.async of the raw tile (8 consecutive threads = one row's
-        // 128 bytes), 3 deep; each thread then reads its own row back from shared memory.
-        // this thread's cp.async units: rows pt/8 + 32 j (j < 4), k-quad pt % 8; the rows' decode
-        // (sample, window origin) is computed once per tile
-        typename Op::RowInfo ri[4];
-        // prefetch cursor (tile, chunk, ring slot), advanced incrementally: no divisions
-        int pf_tile = 0, pf_chunk = 0, pf_slot = 0;
+        typename Op::RowInfo ri[8];
+        // prefetch cursor over this group's chunks (g = grp, grp + 2, ...): tile, chunk, slot
+        int pf_g = grp, pf_tile = 0, pf_chunk = grp, pf_slot = grp, ri_tile = -1;
+        while (pf_chunk >= nchunks) { pf_chunk -= nchunks; ++pf_tile; }
         auto a_issue = [&]() {
-            const int mm0 = (tile0 + pf_tile) * kBM, kk0 = op.kbeg + pf_chunk * kKC;
-            const uint32_t dst = araw + pf_slot * kARawTile;
-            // each warp copies exactly the part of the tile it reads back (rows 32q.., k half h),
-            // so only a warp-level sync separates copy and read
-            if constexpr (Op::AM == 0) {
-                // unit j: row 32q + lane/4 + 8j, k-quad 4h + lane%4 (4 lanes = one row's 64 bytes)
-                if (pf_chunk == 0) {
+            if (pf_g < total) {
+                const int mm0 = (tile0 + pf_tile) * kBM, kk0 = op.kbeg + pf_chunk * kKC;
+                const uint32_t dst = araw + pf_slot * kARawTile;
+                if constexpr (Op::AM == 0) {
+                    // unit j: row 32q + lane/8 + 4j, k-quad lane%8 (8 lanes = one row's 128 bytes)
+                    if (pf_tile != ri_tile) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) ri[j] = op.row_info(mm0 + q * 32 + (lane >> 2) + 8 * j);
-                }
-                const int kq = h * 4 + (lane & 3);
-                const auto tap = op.tap_info(kk0 + kq * 4);
+                        for (int j = 0; j < 8; ++j) ri[j] = op.row_info(mm0 + q * 32 + (lane >> 3) + 4 * j);
+                        ri_tile = pf_tile;
+                    }
+                    const int kq = lane & 7;
+                    const auto tap = op.tap_info(kk0 + kq * 4);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int r = q * 32 + (lane >> 2) + 8 * j;
-                    const float* src = op.a_ptr_tap(ri[j], tap);
+                    for (int j = 0; j < 8; ++j) {
+                        const int r = q * 32 + (lane >> 3) + 4 * j;
+                        const float* src = op.a_ptr_tap(ri[j], tap);
 #ifdef SMX_DBG_NO_LOAD
-                    src = nullptr;
+                        src = nullptr;
 #endif
-                    cp16(dst + (r * kRawLdK + kq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
-                }
-            } else {
-                // MN-contiguous A: unit j = (row quad 8q + lane%8, k = 16h + lane/8 + 4j): 16 bytes =
-                // 4 consecutive rows at one k
-                const int rq = q * 8 + (lane & 7);
-                if (pf_chunk == 0) ri[0] = op.row_info(mm0 + rq * 4);
+                        cp16(dst + r * 128 + ((kq ^ (r & 7)) << 4), src ? src : ctc::kZero16, src ? 16 : 0);
+                    }
+                } else {
+                    // MN-contiguous A: unit j = (row quad 8q + lane%8, k = lane/8 + 4j)
+                    const int rq = q * 8 + (lane & 7);
+                    if (pf_tile != ri_tile) {
+                        ri[0] = op.row_info(mm0 + rq * 4);
+                        ri_tile = pf_tile;
+                    }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int k = h * 16 + (lane >> 3) + 4 * j;
-                    const float* src = op.a_ptr_red(ri[0], op.red_info(kk0 + k));
-                    cp16(dst + (k * kRawLdMN + rq * 4) * 4, src ? src : ctc::kZero16, src ? 16 : 0);
+                    for (int j = 0; j < 8; ++j) {
+                        const int k = (lane >> 3) + 4 * j;
+                        const float* src = op.a_ptr_red(ri[0], op.red_info(kk0 + k));
+                        cp16(dst + k * 512 + rq * 16, src ? src : ctc::kZero16, src ? 16 : 0);
+                    }
                 }
             }
             asm volatile("cp.async.commit_group;");
-            if (++pf_chunk == nchunks) {
-                pf_chunk = 0;
-                ++pf_tile;
-            }
-            if (++pf_slot == kARaw) pf_slot = 0;
+            pf_g += 2;
+            pf_chunk += 2;
+            while (pf_chunk >= nchunks) { pf_chunk -= nchunks; ++pf_tile; }
+            pf_slot += 2;
+            if (pf_slot >= kARaw) pf_slot -= kARaw;
         };
-        for (int gg = 0; gg < kPre; ++gg) {
-            if (gg < total)
-                a_issue();
+        for (int j = 0; j < kDw; ++j) a_issue();
+        int i = 0, c = grp, rd_slot = grp;
+        while (c >= nchunks) { c -= nchunks; ++i; }
+        for (int g = grp; g < total; g += 2) {
+            const int s = g % kStages, u = g / kStages;
+            const int m = (tile0 + i) * kBM + q * 32 + lane;
+            const int k0 = op.kbeg + c * kKC;
+            // B (register path, non-image Ops): the group's 128 threads cover the tile
+            float4 b[8];
+            if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int uu = gt + j * 128, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
+                    b[j] = ld4(kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
+                }
+            } else if constexpr (!Op::B_IMAGE) {
+#pragma unroll
+                for (int v2 = 0; v2 < 2; ++v2) {
+                    const int rq = gt & 31, kq = (gt >> 5) + 4 * v2;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int k = k0 + kq * 4 + j;
+                        b[4 * v2 + j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
+                    }
+                }
+            }
+            // warm L2 with the B rows of this group's chunk kDw + 1 ahead (register-path B)
+            if constexpr (!Op::B_IMAGE) {
+                int pc = c + 2 * (kDw + 1);
+                while (pc >= nchunks) pc -= nchunks;
+                if (g + 2 * (kDw + 1) < total) {
+                    const int pk = op.kbeg + pc * kKC;
+                    if constexpr (Op::BMODE == 1) {  // rows = reduction index: 32 contiguous rows of the tile
+                        const int kk = pk + (gt >> 2);
+                        if (gt < 128 && kk < klim) prefetch_l2(op.b_ptr((gt & 3) * 32, kk));
+                    } else {  // rows = n: one line per 32 k of each row
+                        if (gt < nt && pk < klim) prefetch_l2(op.b_ptr(gt, pk));
+                    }
+                }
+            }
+            float a[32];
+            if constexpr (kDw > 1)
+                asm volatile("cp.async.wait_group %0;" ::"n"(kDw - 1) : "memory");  // own copies of chunk g
             else
-                asm volatile("cp.async.commit_group;");
-        }
-        int g = 0, rd_slot = 0;
-        float4 bn[4];  // next chunk's B registers (non-image Ops)
-        for (int i = 0; i < ntiles; ++i) {
-            const int m0 = (tile0 + i) * kBM;
-            const int m = m0 + q * 32 + lane;
-            const bool mrow = Op::kOnesRow >= 0 ? (m < Op::kOnesRow) : (m < M);
-            for (int c = 0; c < nchunks; ++c, ++g) {
-                const int s = g % kStages, u = g / kStages;
-                const int k0 = op.kbeg + c * kKC;
-                const int ka = k0 + h * 16;
-                // B units (register path, non-image Ops): BMODE 0 -> (row, k-quad), consecutive
-                // threads = consecutive rows; BMODE 1 -> (row-quad, k-quad), 4 rows x 4 k transposed
-                // in registers.  Loaded one chunk ahead (bn) so the global latency overlaps a chunk.
-                const int bunits = Op::BMODE == 0 ? (nt * kKQ + kProducers - 1) / kProducers : 1;
-                auto b_load = [&](int kk0, float4* dst) {
-                    if constexpr (Op::B_IMAGE) {
-                    } else if constexpr (Op::BMODE == 0) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt, k = kk0 + kq * 4;
-                            dst[j] = ld4(j < bunits && kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
-                        }
-                    } else {
-                        const int rq = pt % 32, kq = pt / 32;  // 32 row-quads x 8 k-quads
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int k = kk0 + kq * 4 + j;
-                            dst[j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
-                        }
-                    }
-                };
-                float4 b[4];
-                if (!Op::B_IMAGE) {
-                    if (g == 0) b_load(k0, bn);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) b[j] = bn[j];
-                    if (g + 1 < total) b_load(op.kbeg + ((c + 1 == nchunks) ? 0 : (c + 1)) * kKC, bn);
-                }
-                float a[16];
-                asm volatile("cp.async.wait_group %0;" ::"n"(kPre - 1) : "memory");  // own copies of chunk g landed
-                __syncwarp();  // the warp's copies landed; its reads of chunk g-1's slot are done
-                if (g + kPre < total) a_issue(); else asm volatile("cp.async.commit_group;");
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            {
                 const char* rawg = smem + Plan::ARawOff + rd_slot * kARawTile;
-                if (++rd_slot == kARaw) rd_slot = 0;
+                const int r = q * 32 + lane;
                 if constexpr (Op::AM == 0) {
-                    const float4* rp = reinterpret_cast<const float4*>(rawg + ((q * 32 + lane) * kRawLdK + h * 16) * 4);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float4 t = rp[j];
-                        a[4 * j] = t.x; a[4 * j + 1] = t.y; a[4 * j + 2] = t.z; a[4 * j + 3] = t.w;
+                    for (int kq = 0; kq < 8; ++kq) {
+                        const float4 t = *reinterpret_cast<const float4*>(rawg + r * 128 + ((kq ^ (r & 7)) << 4));
+                        a[4 * kq] = t.x; a[4 * kq + 1] = t.y; a[4 * kq + 2] = t.z; a[4 * kq + 3] = t.w;
                     }
                 } else {
-                    const float* rp = reinterpret_cast<const float*>(rawg) + (h * 16) * kRawLdMN + q * 32 + lane;
+                    const float* rp = reinterpret_cast<const float*>(rawg) + r;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) a[j] = rp[j * kRawLdMN];
+                    for (int k = 0; k < 32; ++k) a[k] = rp[k * 128];
                 }
-                (void)mrow;
-                if (Op::kOnesRow >= 0 && m == Op::kOnesRow) {
+            }
+            __syncwarp();  // this warp's reads of the slot precede the refill below
+            a_issue();
+            rd_slot += 2;
+            if (rd_slot >= kARaw) rd_slot -= kARaw;
+            if (Op::kOnesRow >= 0 && m == Op::kOnesRow) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) a[j] = ka + j < klim ? 1.0f : 0.0f;
+                for (int j = 0; j < 32; ++j) a[j] = k0 + j < klim ? 1.0f : 0.0f;
+            }
+            // ---- wait until the MMAs of this stage's previous use are done
+            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+            char* bh = smem + s * kBStage;
+            char* bl = bh + nt * 128;
+            if constexpr (Op::B_IMAGE) {
+                if (gt == 0) {  // the weight image of this chunk: one bulk copy of hi | lo
+                    mbar_arrive_expect_tx(&full[s], nt * 256);
+                    bulk_g2s(bh, op.b_image(c), nt * 256, &full[s]);
                 }
-                // ---- wait until the MMAs of this stage's previous use are done
-                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-                char* bh = smem + s * kBStage;
-                char* bl = bh + nt * 128;
-                if constexpr (Op::B_IMAGE) {
-                    if (pt == 0) {  // the weight image of this chunk: one bulk copy of hi | lo
-                        mbar_arrive_expect_tx(&full[s], nt * 256);
-                        bulk_g2s(bh, op.b_image(c), nt * 256, &full[s]);
-                    }
-                }
-                // A hi/lo -> TMEM
+            }
+            // A hi/lo -> TMEM (lane = row, column = k)
 #ifndef SMX_DBG_NO_ASTORE
-                {
-                    float lo[16];
+            {
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kABase + s * 64;
+                tmem_st16(ta, a);
+                tmem_st16(ta + 16, a + 16);
+                if (!Op::A_EXACT) {
+                    float lo[32];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) lo[j] = lo_of(a[j]);
-                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + kABase + s * 64 + h * 16;
-                    tmem_st16(ta, a);
-                    if (!Op::A_EXACT) tmem_st16(ta + 32, lo);
+                    for (int j = 0; j < 32; ++j) lo[j] = lo_of(a[j]);
+                    tmem_st16(ta + 32, lo);
+                    tmem_st16(ta + 48, lo + 16);
                 }
+            }
 #endif
-                // B hi/lo -> smem canonical
-                if constexpr (Op::B_IMAGE) {
-                } else if constexpr (Op::BMODE == 0) {
+            // B hi/lo -> smem canonical
+            if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int uu = pt + j * kProducers, r = uu % nt, kq = uu / nt;
-                        if (j < bunits && kq < kKQ) {
-                            const uint32_t off = kq * lbo + (r >> 3) * 128 + (r & 7) * 16;
-                            *reinterpret_cast<float4*>(bh + off) = b[j];
-                            *reinterpret_cast<float4*>(bl + off) =
-                                make_float4(lo_of(b[j].x), lo_of(b[j].y), lo_of(b[j].z), lo_of(b[j].w));
-                        }
+                for (int j = 0; j < 8; ++j) {
+                    const int uu = gt + j * 128, r = uu % nt, kq = uu / nt;
+                    if (kq < kKQ) {
+                        const uint32_t off = kq * lbo + (r >> 3) * 128 + (r & 7) * 16;
+                        *reinterpret_cast<float4*>(bh + off) = b[j];
+                        *reinterpret_cast<float4*>(bl + off) =
+                            make_float4(lo_of(b[j].x), lo_of(b[j].y), lo_of(b[j].z), lo_of(b[j].w));
                     }
-                } else {
-                    const int rq = pt % 32, kq = pt / 32;
+                }
+            } else if constexpr (!Op::B_IMAGE) {
+#pragma unroll
+                for (int v2 = 0; v2 < 2; ++v2) {
+                    const int rq = gt & 31, kq = (gt >> 5) + 4 * v2;
                     if (rq * 4 < nt) {
-                        const float blk[4][4] = {{b[0].x, b[1].x, b[2].x, b[3].x},
-                                                 {b[0].y, b[1].y, b[2].y, b[3].y},
-                                                 {b[0].z, b[1].z, b[2].z, b[3].z},
-                                                 {b[0].w, b[1].w, b[2].w, b[3].w}};
+                        const float4* bb = b + 4 * v2;
+                        const float blk[4][4] = {{bb[0].x, bb[1].x, bb[2].x, bb[3].x},
+                                                 {bb[0].y, bb[1].y, bb[2].y, bb[3].y},
+                                                 {bb[0].z, bb[1].z, bb[2].z, bb[3].z},
+                                                 {bb[0].w, bb[1].w, bb[2].w, bb[3].w}};
 #pragma unroll
                         for (int ii = 0; ii < 4; ++ii) {
                             const int jj = (ii + (rq >> 1)) & 3;
@@ -338,11 +351,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                         }
                     }
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;");
-                asm volatile("fence.proxy.async.shared::cta;");
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive(&full[s]);
             }
+            asm volatile("tcgen05.wait::st.sync.aligned;");
+            asm volatile("fence.proxy.async.shared::cta;");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&full[s]);
+            c += 2;
+            while (c >= nchunks) { c -= nchunks; ++i; }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else if (warp == kMmaWarp) {
@@ -401,13 +416,21 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
         // ================= epilogue =================
         const int q = warp & 3;
         static_assert(Op::kSegChunks > 0, "the epilogue stages every tile in shared memory");
-        float* sacc = reinterpret_cast<float*>(smem + Plan::SaccOff);  // [row][N + 4]
-        constexpr int LD = Plan::SaccLd;
+        float* sacc = reinterpret_cast<float*>(smem + Plan::SaccOff);  // [row][PN], 16-B units swizzled
+        constexpr int PN = Plan::N;
+        // float4 unit (row r, column quad c4) of the tile sums
+        auto s4 = [&](int r, int c4) -> float4* { return reinterpret_cast<float4*>(sacc + r * PN) + (c4 ^ (r & 7)); };
         const int row = q * 32 + lane;
         const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
+            if constexpr (Op::EPI == ctc::kEpiMask) {
+                // warm L2 with the tile's ReLU-mask lines (one 128-byte line per 32 columns of a row)
+                const int m = mt0 + row;
+                if (m < M)
+                    for (int col = 0; col < N; col += 32) prefetch_l2(op.mask_at(m, col));
+            }
             // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
             for (int j = 0; j < nseg; ++j, ++un) {
                 const int acc_i = un & 1, use = un >> 1;
@@ -423,7 +446,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     }
 #pragma unroll
                     for (int jj = 0; jj < 16; jj += 4) {
-                        float4* sp = reinterpret_cast<float4*>(sacc + row * LD + c0 + jj);
+                        float4* sp = s4(row, (c0 + jj) >> 2);
                         const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
                                                       __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
                         if (j == 0) {
@@ -449,7 +472,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     const int r = e / q4, c4 = e % q4, m = mt0 + r;
                     if (m >= M) continue;
                     if (4 * c4 >= N) continue;
-                    float4 x = *reinterpret_cast<const float4*>(sacc + r * LD + 4 * c4);
+                    float4 x = *s4(r, c4);
                     if constexpr (Op::EPI != ctc::kEpiStore) {
                         const float4 b = op.bias4(4 * c4);
                         x.x = __fadd_rn(x.x, b.x); x.y = __fadd_rn(x.y, b.y);
@@ -465,7 +488,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                 // transposed outputs: lanes = consecutive rows of one column (coalesced)
                 const int m = mt0 + row;
                 if (m < M)
-                    for (int col = 0; col < N; ++col) *op.ct_at(col, m) = sacc[row * LD + col];
+                    for (int col = 0; col < N; ++col)
+                        *op.ct_at(col, m) = sacc[row * PN + (((col >> 2) ^ (row & 7)) << 2) + (col & 3)];
             } else {
                 // ReLU-masked scatter to the 4 sub-pixels, cooperative: thread = fixed float4 column
                 // (class, 4 channels), rows r0, r0 + 4, ...; a warp covers one row's N columns =
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (off[u] < 0) continue;
-                        const float4 x = *reinterpret_cast<const float4*>(sacc + (r0 + RSTEP * (i0 + u)) * LD + 4 * c4);
+                        const float4 x = *s4(r0 + RSTEP * (i0 + u), c4);
                         op.store_masked(mt0 + r0 + RSTEP * (i0 + u), 4 * c4, off[u],
                             make_float4(mk[u].x > 0.0f ? x.x : 0.0f, mk[u].y > 0.0f ? x.y : 0.0f,
                                         mk[u].z > 0.0f ? x.z : 0.0f, mk[u].w > 0.0f ? x.w : 0.0f));

@@ -99,6 +99,7 @@ struct DenseOp {
             for (int j = 0; j < 4 && col + j < N; ++j) c[j] = v[j];
         }
     }
+    __device__ __forceinline__ const float* mask_at(int m, int col) const { return mask + (long long)m * ldmask + n0 + col; }
     __device__ __forceinline__ long long mask_off(int m, int col) const {
         return (long long)m * ldmask + n0 + col;
     }
