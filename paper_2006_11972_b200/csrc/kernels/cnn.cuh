@@ -742,58 +742,84 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
 // These kernels use plain fp32 FMA (at least as accurate as 3xTF32) in their own fixed order;
 // exact mode keeps the oracle-order kernels above.
 
-// One thread per output pixel, all 32 channels in registers; W1^T staged in shared memory and
-// read as warp-uniform broadcasts.  grid (ceil(max_batch*1024/256), groups), block 256.
+// Register-blocked: one thread = 4 consecutive output pixels of a row x 16 output channels (64
+// accumulators), so each shared-memory weight vector feeds 16 FMAs and each input float4 of the
+// 3 x 6 window feeds up to 3 taps x 4 pixels.  W1^T staged in shared memory ([27][32], read as
+// warp-uniform broadcasts); outputs staged in shared memory and written back as contiguous 16-B
+// stores.  grid (ceil(max_batch * 1024 / 512), groups), block 256 (512 pixels = half a sample).
 __global__ void __launch_bounds__(256) conv1_fwd_fast(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     __shared__ __align__(16) float wt[27][32];
     __shared__ float bs_[32];
-    __shared__ __align__(16) float stage[256 * 36];  // 256 pixels x (32 + 4 pad) floats
+    __shared__ __align__(16) float stage[256 * 36];  // 256 pixels x (32 + 4 pad) floats, two passes
+    if (blockIdx.x * 512 >= v.bs * 1024) return;
     for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
         const int co = i & 31, k = i >> 5, t = k / 3, ci = k % 3;
         wt[k][co] = v.w[Geo<1>::OffW + (co * 9 + t) * 4 + ci];
     }
     if (threadIdx.x < 32) bs_[threadIdx.x] = v.w[Geo<1>::OffB + threadIdx.x];
     __syncthreads();
-    if (blockIdx.x * blockDim.x >= v.bs * 1024) return;
-    const int m = min(blockIdx.x * blockDim.x + threadIdx.x, v.bs * 1024 - 1);  // tail threads recompute
     const float* in = layer_in<1>(p, v);
-    const int n = m >> 10, oh = (m >> 5) & 31, ow = m & 31;
-    float acc[32];
+    const int hh = threadIdx.x & 1;                 // channel half: co in [16 hh, 16 hh + 16)
+    const int pq = blockIdx.x * 128 + (threadIdx.x >> 1);  // pixel quad (4 pixels of one row)
+    const int m0 = pq * 4;                           // first pixel (always < bs * 1024: 1024 % 512 == 0)
+    const int n = m0 >> 10, oh = (m0 >> 5) & 31, ow0 = m0 & 31;
+    float acc[4][16];
 #pragma unroll
-    for (int co = 0; co < 32; ++co) acc[co] = bs_[co];
+    for (int px = 0; px < 4; ++px)
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
-        const int ih = oh + t / 3 - 1, iw = ow + t % 3 - 1;
-        if ((unsigned)ih >= 32u || (unsigned)iw >= 32u) continue;
-        const float4 x = __ldg(reinterpret_cast<const float4*>(in + (((n << 5) + ih) * 32 + iw) * 4));
-        const float xv[3] = {x.x, x.y, x.z};
+        for (int c = 0; c < 16; ++c) acc[px][c] = bs_[16 * hh + c];
 #pragma unroll
-        for (int ci = 0; ci < 3; ++ci) {
-            const float4* wr = reinterpret_cast<const float4*>(wt[t * 3 + ci]);
+    for (int dh = 0; dh < 3; ++dh) {
+        const int ih = oh + dh - 1;
+        if ((unsigned)ih >= 32u) continue;
+        float4 xr[6];  // input columns ow0 - 1 .. ow0 + 4
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-                const float4 w4 = wr[c4];
-                acc[4 * c4] = __fmaf_rn(xv[ci], w4.x, acc[4 * c4]);
-                acc[4 * c4 + 1] = __fmaf_rn(xv[ci], w4.y, acc[4 * c4 + 1]);
-                acc[4 * c4 + 2] = __fmaf_rn(xv[ci], w4.z, acc[4 * c4 + 2]);
-                acc[4 * c4 + 3] = __fmaf_rn(xv[ci], w4.w, acc[4 * c4 + 3]);
+        for (int j = 0; j < 6; ++j) {
+            const int iw = ow0 + j - 1;
+            xr[j] = (unsigned)iw < 32u ? __ldg(reinterpret_cast<const float4*>(in + (((n << 5) + ih) * 32 + iw) * 4))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int dw = 0; dw < 3; ++dw) {
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) {
+                const float4* wr = reinterpret_cast<const float4*>(&wt[(dh * 3 + dw) * 3 + ci][16 * hh]);
+                const float4 w0 = wr[0], w1 = wr[1], w2 = wr[2], w3 = wr[3];
+                const float wv[16] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w,
+                                      w2.x, w2.y, w2.z, w2.w, w3.x, w3.y, w3.z, w3.w};
+#pragma unroll
+                for (int px = 0; px < 4; ++px) {
+                    const float4 xv4 = xr[px + dw];
+                    const float xv = ci == 0 ? xv4.x : ci == 1 ? xv4.y : xv4.z;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) acc[px][c] = __fmaf_rn(xv, wv[c], acc[px][c]);
+                }
             }
         }
     }
-    // stage the block's 256 x 32 outputs in shared memory (row stride 33 float4-quads... padded) and
-    // write them back as contiguous 16-byte stores
-    __syncthreads();  // wt no longer needed: reuse nothing, stage separately
-    float4* st = reinterpret_cast<float4*>(stage) + threadIdx.x * 9;
+    // two passes of 256 pixels (threads 0-127, then 128-255) through the staging buffer
+    const int m_first = blockIdx.x * 512;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        __syncthreads();
+        if ((threadIdx.x >> 7) == pass) {
 #pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4)
-        st[c4] = make_float4(fmaxf(acc[4 * c4], 0.0f), fmaxf(acc[4 * c4 + 1], 0.0f), fmaxf(acc[4 * c4 + 2], 0.0f),
-                             fmaxf(acc[4 * c4 + 3], 0.0f));
-    __syncthreads();
-    const int m_first = blockIdx.x * blockDim.x;
-    const int rows = min((int)blockDim.x, v.bs * 1024 - m_first);
-    float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)m_first * 32);
-    for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) out[i] = reinterpret_cast<float4*>(stage)[(i >> 3) * 9 + (i & 7)];
+            for (int px = 0; px < 4; ++px) {
+                float4* st = reinterpret_cast<float4*>(stage + (((threadIdx.x & 127) >> 1) * 4 + px) * 36 + 16 * hh);
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4)
+                    st[c4] = make_float4(fmaxf(acc[px][4 * c4], 0.0f), fmaxf(acc[px][4 * c4 + 1], 0.0f),
+                                         fmaxf(acc[px][4 * c4 + 2], 0.0f), fmaxf(acc[px][4 * c4 + 3], 0.0f));
+            }
+        }
+        __syncthreads();
+        const int base = m_first + pass * 256;
+        const int rows = min(256, v.bs * 1024 - base);
+        float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)base * 32);
+        for (int i = threadIdx.x; i < rows * 8; i += blockDim.x)
+            out[i] = reinterpret_cast<float4*>(stage)[(i >> 3) * 9 + (i & 7)];
+    }
 }
 
 // Per-sample partial weight gradient of conv1: block = one (sample, slot); lane = output channel,
@@ -819,22 +845,35 @@ __global__ void __launch_bounds__(256) conv1_wgrad_fast(ConvArgs p) {
     float acc[28];
 #pragma unroll
     for (int j = 0; j < 28; ++j) acc[j] = 0.0f;
+    // 4 consecutive pixels of a row per step: their 3 x 6 input window (18 broadcast float4 loads)
+    // feeds 4 x 27 FMAs per lane
     for (int p0 = warp * 128; p0 < warp * 128 + 128; p0 += 8) {
         float dv[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) dv[e] = __ldg(dy + (p0 + e) * 32 + co);  // 8 loads in flight
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int pix = p0 + e, oh = pix >> 5, ow = pix & 31;
-            const float d = dv[e];
+        for (int hq = 0; hq < 2; ++hq) {
+            const int pix0 = p0 + 4 * hq, oh = pix0 >> 5, ow0 = pix0 & 31;
 #pragma unroll
-            for (int t = 0; t < 9; ++t) {
-                const float4 x = reinterpret_cast<const float4*>(img)[(oh + t / 3) * 34 + ow + t % 3];
-                acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
-                acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
-                acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
+            for (int dh = 0; dh < 3; ++dh) {
+                float4 xr[6];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) xr[j] = reinterpret_cast<const float4*>(img)[(oh + dh) * 34 + ow0 + j];
+#pragma unroll
+                for (int px = 0; px < 4; ++px) {
+                    const float d = dv[4 * hq + px];
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw) {
+                        const float4 x = xr[px + dw];
+                        const int t = dh * 3 + dw;
+                        acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
+                        acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
+                        acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
+                    }
+                }
             }
-            acc[27] = __fadd_rn(acc[27], d);
+#pragma unroll
+            for (int px = 0; px < 4; ++px) acc[27] = __fadd_rn(acc[27], dv[4 * hq + px]);
         }
     }
 #pragma unroll

@@ -99,6 +99,12 @@ __device__ __forceinline__ void split1(float a, float& h, float& l) {
     l = tf32_rna(__fsub_rn(a, h));
 }
 
+#ifdef SMX_DBG_NO_BREG
+constexpr bool kDbgNoBreg = true;  // profiling variant: skip the register-path B operand
+#else
+constexpr bool kDbgNoBreg = false;
+#endif
+
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -212,6 +218,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     for (int j = 0; j < 8; ++j) {
                         const int k = (lane >> 3) + 4 * j;
                         const float* src = op.a_ptr_red(ri[0], op.red_info(kk0 + k));
+#ifdef SMX_DBG_NO_LOAD
+                        src = nullptr;
+#endif
                         cp16(dst + k * 512 + rq * 16, src ? src : ctc::kZero16, src ? 16 : 0);
                     }
                 }
@@ -232,13 +241,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
             const int k0 = op.kbeg + c * kKC;
             // B (register path, non-image Ops): the group's 128 threads cover the tile
             float4 b[8];
+#ifdef SMX_DBG_NO_BREG
+            if constexpr (false) {
+#else
             if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
+#endif
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int uu = gt + j * 128, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
                     b[j] = ld4(kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
                 }
-            } else if constexpr (!Op::B_IMAGE) {
+            } else if constexpr (!Op::B_IMAGE && !kDbgNoBreg) {
 #pragma unroll
                 for (int v2 = 0; v2 < 2; ++v2) {
                     const int rq = gt & 31, kq = (gt >> 5) + 4 * v2;
@@ -318,7 +331,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
             }
 #endif
             // B hi/lo -> smem canonical
-            if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
+            if constexpr (kDbgNoBreg) {
+            } else if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int uu = gt + j * 128, r = uu % nt, kq = uu / nt;
