@@ -232,6 +232,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
             pf_slot += 2;
             if (pf_slot >= kARaw) pf_slot -= kARaw;
         };
+#ifdef SMX_DBG_MMA_ONLY
+        // profiling variant: producers only hand stages to the MMA (B image still copied)
+        for (int g = grp; g < total; g += 2) {
+            const int s = g % kStages, u = g / kStages;
+            if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+            if constexpr (Op::B_IMAGE) {
+                if (gt == 0) {
+                    int cc = g % nchunks;
+                    mbar_arrive_expect_tx(&full[s], nt * 256);
+                    bulk_g2s(smem + s * kBStage, op.b_image(cc), nt * 256, &full[s]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&full[s]);
+        }
+#else
         for (int j = 0; j < kDw; ++j) a_issue();
         int i = 0, c = grp, rd_slot = grp;
         while (c >= nchunks) { c -= nchunks; ++i; }
@@ -373,6 +389,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
             c += 2;
             while (c >= nchunks) { c -= nchunks; ++i; }
         }
+#endif
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
@@ -399,24 +416,38 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
                     const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
                     const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
-#ifdef SMX_DBG_NO_MMA
-                    for (int st = 0; st < 0; ++st) {
-#else
-                    for (int st = 0; st < ksteps; ++st) {
-#endif
-                        const uint32_t o = st * 2 * lbo;
-                        const uint64_t dbh = smem_desc(bhi + o, lbo, 128), dbl = smem_desc(blo + o, lbo, 128);
-                        uint32_t accum = (unit_start && st == 0) ? 0u : 1u;
-                        if (!Op::A_EXACT) {
-                            mma_ts(dacc, alo + st * 8, dbh, idesc, accum);
-                            accum = 1u;
+                    // descriptors built once per chunk; a k-step of 8 tf32 advances the B tiles by
+                    // 2 LBO (the 14-bit address field cannot overflow below 256 KB of smem)
+                    const uint64_t dbh0 = smem_desc(bhi, lbo, 128), dbl0 = smem_desc(blo, lbo, 128);
+                    const uint64_t dstep = (uint64_t)((2 * lbo) >> 4);
+#ifndef SMX_DBG_NO_MMA
+                    if (ksteps == 4) {
+#pragma unroll
+                        for (int st = 0; st < 4; ++st) {
+                            const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
+                            const uint32_t a_off = st * 8;
+                            if (!Op::A_EXACT) mma_ts(dacc, alo + a_off, dbh, idesc, (unit_start && st == 0) ? 0u : 1u);
+                            if (!Op::B_EXACT)
+                                mma_ts(dacc, ahi + a_off, dbl, idesc, (unit_start && st == 0 && Op::A_EXACT) ? 0u : 1u);
+                            mma_ts(dacc, ahi + a_off, dbh, idesc,
+                                   (unit_start && st == 0 && Op::A_EXACT && Op::B_EXACT) ? 0u : 1u);
                         }
-                        if (!Op::B_EXACT) {
-                            mma_ts(dacc, ahi + st * 8, dbl, idesc, accum);
-                            accum = 1u;
+                    } else {
+                        for (int st = 0; st < ksteps; ++st) {
+                            const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
+                            uint32_t accum = (unit_start && st == 0) ? 0u : 1u;
+                            if (!Op::A_EXACT) {
+                                mma_ts(dacc, alo + st * 8, dbh, idesc, accum);
+                                accum = 1u;
+                            }
+                            if (!Op::B_EXACT) {
+                                mma_ts(dacc, ahi + st * 8, dbl, idesc, accum);
+                                accum = 1u;
+                            }
+                            mma_ts(dacc, ahi + st * 8, dbh, idesc, accum);
                         }
-                        mma_ts(dacc, ahi + st * 8, dbh, idesc, accum);
                     }
+#endif
                     mma_commit(&empty[s]);
                     if (unit_end) {
                         mma_commit(&accf[acc_i]);
