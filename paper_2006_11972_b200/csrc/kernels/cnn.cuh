@@ -16,6 +16,11 @@
 #include "gemm_tc.cuh"
 #include "step_kernels.cuh"
 
+// chunks (of 32 products) per TMEM accumulation segment before the fp32 promotion (§3b.5)
+#ifndef SMX_SEG_CHUNKS
+#define SMX_SEG_CHUNKS 4
+#endif
+
 namespace smx {
 namespace cnn {
 
@@ -457,7 +462,7 @@ struct Fwd {
     using G = Geo<L>;
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS;
     const float* in;
     const float* w;
     const float* bias;
@@ -537,7 +542,7 @@ struct Dgrad {
     static_assert(G::S == 2, "sub-pixel decomposition is for stride 2");
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS;
     static constexpr int HH = G::H / 2;  // == OH
     const float* dy;
     const float* w;
@@ -621,16 +626,20 @@ struct Wgrad {
     }
     // per-chunk decode of a reduction index (sample, output pixel), then the row quad's pointer
     struct RedInfo {
-        int base, ih, iw;
+        int base, ih, iw, left;  // first pixel of a run; `left` reduction indices remain in range
     };
     __device__ __forceinline__ RedInfo red_info(int m) const {
-        if (m >= kbeg + K) return RedInfo{0, -1000, -1000};
+        if (m >= kbeg + K) return RedInfo{0, -1000, -1000, 0};
         const int n = m / (G::OH * G::OH), pix = m % (G::OH * G::OH);
-        return RedInfo{n * G::H * G::H * G::Ci, (pix / G::OH) * G::S, (pix % G::OH) * G::S};
+        return RedInfo{n * G::H * G::H * G::Ci, (pix / G::OH) * G::S, (pix % G::OH) * G::S, kbeg + K - m};
     }
     __device__ __forceinline__ const float* a_ptr_red(const RowInfo& ri, const RedInfo& rd) const {
-        const int ih = rd.ih + ri.kh, iw = rd.iw + ri.kw;
-        if ((unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H) return nullptr;
+        return a_ptr_red_step(ri, rd, 0);
+    }
+    // reduction index m + j of a run of 8 that starts at a multiple of 8 (same output row: OH % 8 == 0)
+    __device__ __forceinline__ const float* a_ptr_red_step(const RowInfo& ri, const RedInfo& rd, int j) const {
+        const int ih = rd.ih + ri.kh, iw = rd.iw + G::S * j + ri.kw;
+        if (j >= rd.left || (unsigned)ih >= (unsigned)G::H || (unsigned)iw >= (unsigned)G::H) return nullptr;
         return in + (rd.base + (ih * G::H + iw) * G::Ci + ri.ci);
     }
     // the 4 rows of `ri` at reduction index m (sample, output pixel)
@@ -641,7 +650,7 @@ struct Wgrad {
         return in + ((n * G::H + ih) * G::H + iw) * G::Ci + ri.ci;
     }
     __device__ __forceinline__ const float* b_image(int) const { return nullptr; }
-    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld, kSegChunks = 4;
+    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld, kSegChunks = SMX_SEG_CHUNKS;
     const float* in;
     const float* dy;
     float* part;

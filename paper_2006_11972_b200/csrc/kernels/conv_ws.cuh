@@ -105,6 +105,21 @@ constexpr bool kDbgNoBreg = true;  // profiling variant: skip the register-path 
 constexpr bool kDbgNoBreg = false;
 #endif
 
+// MMA issue from a whole warp: descriptors stay warp-uniform (uniform registers, no per-MMA
+// R2UR moves) and elect.sync picks the issuing lane.  Measured (profiles/micro/mma_rate.cu):
+// 12 tf32 MMAs per chunk at N = 64 take 384 cycles this way vs ~870 from a single thread.
+__device__ __forceinline__ void mma_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)));
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -208,16 +223,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                         cp16(dst + r * 128 + ((kq ^ (r & 7)) << 4), src ? src : ctc::kZero16, src ? 16 : 0);
                     }
                 } else {
-                    // MN-contiguous A: unit j = (row quad 8q + lane%8, k = lane/8 + 4j)
+                    // MN-contiguous A: unit j = (row quad 8q + lane%8, k = 8 (lane/8) + j): each lane walks
+                    // 8 consecutive reduction indices (one decode, then a pointer stride)
                     const int rq = q * 8 + (lane & 7);
                     if (pf_tile != ri_tile) {
                         ri[0] = op.row_info(mm0 + rq * 4);
                         ri_tile = pf_tile;
                     }
+                    const int kb = (lane >> 3) * 8;
+                    const auto rd = op.red_info(kk0 + kb);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int k = (lane >> 3) + 4 * j;
-                        const float* src = op.a_ptr_red(ri[0], op.red_info(kk0 + k));
+                        const int k = kb + j;
+                        const float* src = op.a_ptr_red_step(ri[0], rd, j);
 #ifdef SMX_DBG_NO_LOAD
                         src = nullptr;
 #endif
@@ -268,13 +286,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     b[j] = ld4(kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
                 }
             } else if constexpr (!Op::B_IMAGE && !kDbgNoBreg) {
+                // units (row quad, k quad) spread over all 128 threads of the group
+                const int nq = nt >> 2;
 #pragma unroll
                 for (int v2 = 0; v2 < 2; ++v2) {
-                    const int rq = gt & 31, kq = (gt >> 5) + 4 * v2;
+                    const int uu = gt + 128 * v2, rq = uu % nq, kq = uu / nq;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const int k = k0 + kq * 4 + j;
-                        b[4 * v2 + j] = ld4(rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
+                        b[4 * v2 + j] = ld4(kq < kKQ && rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
                     }
                 }
             }
@@ -360,10 +380,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                     }
                 }
             } else if constexpr (!Op::B_IMAGE) {
+                const int nq = nt >> 2;
 #pragma unroll
                 for (int v2 = 0; v2 < 2; ++v2) {
-                    const int rq = gt & 31, kq = (gt >> 5) + 4 * v2;
-                    if (rq * 4 < nt) {
+                    const int uu = gt + 128 * v2, rq = uu % nq, kq = uu / nq;
+                    if (kq < kKQ) {
                         const float4* bb = b + 4 * v2;
                         const float blk[4][4] = {{bb[0].x, bb[1].x, bb[2].x, bb[3].x},
                                                  {bb[0].y, bb[1].y, bb[2].y, bb[3].y},
@@ -392,8 +413,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
 #endif
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else if (warp == kMmaWarp) {
-        // ================= MMA issuer =================
-        if (lane == 0) {
+        // ================= MMA issuer (whole warp, elected lane issues) =================
+        {
             const uint32_t idesc = idesc_tf32(nt);
             const uint32_t smem_base = smem_u32(smem);
             int g = 0, un = 0;
@@ -426,10 +447,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                         for (int st = 0; st < 4; ++st) {
                             const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
                             const uint32_t a_off = st * 8;
-                            if (!Op::A_EXACT) mma_ts(dacc, alo + a_off, dbh, idesc, (unit_start && st == 0) ? 0u : 1u);
+                            if (!Op::A_EXACT) mma_ts_e(dacc, alo + a_off, dbh, idesc, (unit_start && st == 0) ? 0u : 1u);
                             if (!Op::B_EXACT)
-                                mma_ts(dacc, ahi + a_off, dbl, idesc, (unit_start && st == 0 && Op::A_EXACT) ? 0u : 1u);
-                            mma_ts(dacc, ahi + a_off, dbh, idesc,
+                                mma_ts_e(dacc, ahi + a_off, dbl, idesc, (unit_start && st == 0 && Op::A_EXACT) ? 0u : 1u);
+                            mma_ts_e(dacc, ahi + a_off, dbh, idesc,
                                    (unit_start && st == 0 && Op::A_EXACT && Op::B_EXACT) ? 0u : 1u);
                         }
                     } else {
@@ -437,20 +458,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                             const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
                             uint32_t accum = (unit_start && st == 0) ? 0u : 1u;
                             if (!Op::A_EXACT) {
-                                mma_ts(dacc, alo + st * 8, dbh, idesc, accum);
+                                mma_ts_e(dacc, alo + st * 8, dbh, idesc, accum);
                                 accum = 1u;
                             }
                             if (!Op::B_EXACT) {
-                                mma_ts(dacc, ahi + st * 8, dbl, idesc, accum);
+                                mma_ts_e(dacc, ahi + st * 8, dbl, idesc, accum);
                                 accum = 1u;
                             }
-                            mma_ts(dacc, ahi + st * 8, dbh, idesc, accum);
+                            mma_ts_e(dacc, ahi + st * 8, dbh, idesc, accum);
                         }
                     }
 #endif
-                    mma_commit(&empty[s]);
+                    mma_commit_e(&empty[s]);
                     if (unit_end) {
-                        mma_commit(&accf[acc_i]);
+                        mma_commit_e(&accf[acc_i]);
                         ++un;
                     }
                 }

@@ -24,7 +24,7 @@ struct DenseOp {
     using Args = GemmArgs;
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
     static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = 4;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS;
     const float* A;
     const float* B;
     float* C;
@@ -75,9 +75,12 @@ struct DenseOp {
     struct RedInfo {
         int k;
     };
-    __device__ __forceinline__ RedInfo red_info(int k) const { return RedInfo{k < K ? k : -1}; }
+    __device__ __forceinline__ RedInfo red_info(int k) const { return RedInfo{k}; }
     __device__ __forceinline__ const float* a_ptr_red(const RowInfo& r, const RedInfo& d) const {
-        return (r.ptr && d.k >= 0) ? r.ptr + (long long)d.k * lda : nullptr;
+        return a_ptr_red_step(r, d, 0);
+    }
+    __device__ __forceinline__ const float* a_ptr_red_step(const RowInfo& r, const RedInfo& d, int j) const {
+        return (r.ptr && d.k + j < K) ? r.ptr + (long long)(d.k + j) * lda : nullptr;
     }
     // ---- B (register path): BMODE 0 -> 4 consecutive k of row n; BMODE 1 -> rows n..n+3 at k
     __device__ __forceinline__ const float* b_ptr(int n, int k) const {
