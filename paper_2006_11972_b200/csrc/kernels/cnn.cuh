@@ -601,10 +601,10 @@ struct Dgrad {
     // masked epilogue: mask and output share the offset (input pixel, channel)
     __device__ __forceinline__ long long mask_off(int r, int col) const { return pix_off(r, col); }
     __device__ __forceinline__ float4 mask4(long long off) const {
-        return __ldg(reinterpret_cast<const float4*>(act + off));
+        return __ldcs(reinterpret_cast<const float4*>(act + off));  // last use of the activation here
     }
     __device__ __forceinline__ void store_masked(int, int, long long off, float4 x) const {
-        *reinterpret_cast<float4*>(dx + off) = x;
+        __stcs(reinterpret_cast<float4*>(dx + off), x);  // streaming: read next by another kernel
     }
 };
 
