@@ -462,7 +462,7 @@ struct Fwd {
     using G = Geo<L>;
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = L == 3 ? 8 : 4;
     const float* in;
     const float* w;
     const float* bias;
@@ -542,7 +542,7 @@ struct Dgrad {
     static_assert(G::S == 2, "sub-pixel decomposition is for stride 2");
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
     const float* dy;
     const float* w;
@@ -650,7 +650,7 @@ struct Wgrad {
         return in + ((n * G::H + ih) * G::H + iw) * G::Ci + ri.ci;
     }
     __device__ __forceinline__ const float* b_image(int) const { return nullptr; }
-    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld, kSegChunks = SMX_SEG_CHUNKS;
+    static constexpr int kOnesRow = 9 * G::Ci, kPartLd = Part<L>::Ld, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;
     const float* in;
     const float* dy;
     float* part;

@@ -34,9 +34,8 @@ using namespace smx::tc3;
 
 constexpr int kMaxStages = 4;                    // B smem / A TMEM ring (TMEM: 4 x 64 columns)
 constexpr int kProducers = 256;                  // warps 0-7
-constexpr int kEpiWarp0 = 8;                     // warps 8-11
-constexpr int kMmaWarp = 12;
-constexpr int kWsThreads = 13 * 32;
+constexpr int kEpiWarp0 = 8;                     // warps 8.. : Op::kEpiWarps epilogue warps (4 or 8),
+                                                 // then the MMA warp
 constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K-major canonical, N <= 128
 constexpr int kARawTile = kBM * kKC * 4;         // raw A tile, 16 KB: [128 rows][32 k] (16-B units
                                                  // XOR-swizzled by row) or [32 k][128 rows]
@@ -60,6 +59,12 @@ struct WsPlan {
     static constexpr int BarOff = ARawOff + ARaw * kARawTile;
     static constexpr int SaccOff = BarOff + 128;
     static constexpr int Bytes = SaccOff + Sacc;
+    // epilogue: one warp per TMEM lane quadrant (4), or two each draining half the columns (8)
+    static constexpr int EpiWarps = Op::kEpiWarps;
+    static_assert(EpiWarps == 4 || EpiWarps == 8, "epilogue warps");
+    static constexpr int EpiThreads = EpiWarps * 32;
+    static constexpr int MmaWarp = kEpiWarp0 + EpiWarps;
+    static constexpr int Threads = (MmaWarp + 1) * 32;
 };
 template <class Op>
 constexpr int ws_smem() {
@@ -141,7 +146,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ float lo_of(float a) { return __fsub_rn(a, __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
 
 template <class Op>
-__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Args p, int tiles) {
+__global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typename Op::Args p, int tiles) {
     extern __shared__ __align__(1024) char smem[];
     using Plan = WsPlan<Op>;
     constexpr int kBStage = Plan::BStage, kARaw = Plan::ARaw, kPre = Plan::ARaw - 1;  // prefetch distance
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&accf[a], 1);
-            mbar_init(&acce[a], 128);
+            mbar_init(&acce[a], Plan::EpiThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
         }
 #endif
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-    } else if (warp == kMmaWarp) {
+    } else if (warp == Plan::MmaWarp) {
         // ================= MMA issuer (whole warp, elected lane issues) =================
         {
             const uint32_t idesc = idesc_tf32(nt);
@@ -480,14 +485,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
         __syncwarp();
     } else {
         // ================= epilogue =================
-        const int q = warp & 3;
+        const int q = warp & 3, ch = (warp - kEpiWarp0) >> 2;  // lane quadrant, column half
         static_assert(Op::kSegChunks > 0, "the epilogue stages every tile in shared memory");
         float* sacc = reinterpret_cast<float*>(smem + Plan::SaccOff);  // [row][PN], 16-B units swizzled
         constexpr int PN = Plan::N;
         // float4 unit (row r, column quad c4) of the tile sums
         auto s4 = [&](int r, int c4) -> float4* { return reinterpret_cast<float4*>(sacc + r * PN) + (c4 ^ (r & 7)); };
         const int row = q * 32 + lane;
-        const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+        const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..EpiThreads-1
+        // this warp's accumulator columns: half of the tile (all of it below 32 columns)
+        const bool halves = Plan::EpiWarps == 8 && nt >= 32;
+        const int cw = halves ? nt / 2 : (ch == 0 ? nt : 0), cbeg = halves ? ch * cw : 0;
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
@@ -495,18 +503,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                 // warm L2 with the tile's ReLU-mask lines (one 128-byte line per 32 columns of a row)
                 const int m = mt0 + row;
                 if (m < M)
-                    for (int col = 0; col < N; col += 32) prefetch_l2(op.mask_at(m, col));
+                    for (int col = 32 * ch; col < N; col += 32 * (Plan::EpiWarps / 4)) prefetch_l2(op.mask_at(m, col));
             }
             // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
             for (int j = 0; j < nseg; ++j, ++un) {
                 const int acc_i = un & 1, use = un >> 1;
                 mbar_wait(&accf[acc_i], use & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                for (int c0 = 0; c0 < nt; c0 += 16) {
+                if (cw == 0) {  // nothing to drain for this warp: release at once
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&acce[acc_i]);
+                }
+                for (int c0 = cbeg; c0 < cbeg + cw; c0 += 16) {
                     uint32_t r[16];
                     tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
                     asm volatile("tcgen05.wait::ld.sync.aligned;");
-                    if (c0 + 16 >= nt) {
+                    if (c0 + 16 >= cbeg + cw) {
                         asm volatile("tcgen05.fence::before_thread_sync;");
                         mbar_arrive(&acce[acc_i]);
                     }
@@ -532,9 +544,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
             if constexpr (Op::EPI == ctc::kEpiBiasRelu || Op::EPI == ctc::kEpiBias || Op::EPI == ctc::kEpiStore) {
                 // row-major output tile: cooperative, coalesced write-out, consecutive threads =
                 // consecutive 16 bytes of a row
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // the whole tile is in sacc
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // the whole tile is in sacc
                 const int q4 = N / 4;
-                for (int e = et; e < kBM * q4; e += 128) {
+                for (int e = et; e < kBM * q4; e += Plan::EpiThreads) {
                     const int r = e / q4, c4 = e % q4, m = mt0 + r;
                     if (m >= M) continue;
                     if (4 * c4 >= N) continue;
@@ -549,20 +561,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                                         x.w > 0.0f ? x.w : 0.0f);
                     op.store4(m, 4 * c4, x);
                 }
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // sacc free for the next tile
             } else if constexpr (Op::EPI == ctc::kEpiPartT) {
                 // transposed outputs: lanes = consecutive rows of one column (coalesced)
                 const int m = mt0 + row;
-                if (m < M)
-                    for (int col = 0; col < N; ++col)
+                if (m < M)  // each warp writes the columns it drained (no barrier needed)
+                    for (int col = cbeg; col < min(N, cbeg + cw); ++col)
                         *op.ct_at(col, m) = sacc[row * PN + (((col >> 2) ^ (row & 7)) << 2) + (col & 3)];
             } else {
                 // ReLU-masked scatter to the 4 sub-pixels, cooperative: thread = fixed float4 column
                 // (class, 4 channels), rows r0, r0 + 4, ...; a warp covers one row's N columns =
                 // whole 128-byte pixel segments.  Mask loads are issued 8 rows ahead of their use.
-                constexpr int Q4 = Plan::N / 4, RSTEP = 128 / Q4, PER = kBM / RSTEP, U = 8;
-                static_assert(128 % Q4 == 0 && PER % U == 0, "epilogue mapping");
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // the whole tile is in sacc
+                constexpr int Q4 = Plan::N / 4, RSTEP = Plan::EpiThreads / Q4, PER = kBM / RSTEP, U = 8;
+                static_assert(Plan::EpiThreads % Q4 == 0 && PER % U == 0, "epilogue mapping");
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // the whole tile is in sacc
                 const int c4 = et % Q4, r0 = et / Q4;
                 for (int i0 = 0; i0 < PER; i0 += U) {
                     float4 mk[U];
@@ -582,7 +594,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(typename Op::Arg
                                         mk[u].z > 0.0f ? x.z : 0.0f, mk[u].w > 0.0f ? x.w : 0.0f));
                     }
                 }
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // sacc free for the next tile
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // sacc free for the next tile
             }
 #endif
         }

@@ -134,7 +134,7 @@ void dense_ws_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
     }
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
     dim3 grid((a.N + 127) / 128, mtiles, groups);
-    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::kWsThreads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, 1);
+    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::WsPlan<Op>::Threads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, 1);
     launch_check(c, "dense_ws");
 }
 
@@ -229,7 +229,7 @@ void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) 
     int tpc = conv_tpc<Op>();
     while (tpc > 1 && (long long)gx * ((mtiles + tpc - 1) / tpc) * groups < 2 * 148) tpc /= 2;
     dim3 grid(gx, (mtiles + tpc - 1) / tpc, groups);
-    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::kWsThreads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, tpc);
+    cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::WsPlan<Op>::Threads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, tpc);
     launch_check(c, "conv_ws");
 }
 
