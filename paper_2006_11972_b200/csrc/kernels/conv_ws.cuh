@@ -291,16 +291,17 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     b[j] = ld4(kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
                 }
             } else if constexpr (!Op::B_IMAGE && !kDbgNoBreg) {
-                // units (row quad, k quad) spread over all 128 threads of the group
-                const int nq = nt >> 2;
+                // MN-contiguous B: unit (row r, k quad) = 4 scalar loads down the reduction index;
+                // lanes = consecutive rows, so each load is one coalesced 128-byte line and the
+                // unit is already the K-major 16-byte group (no transpose)
 #pragma unroll
-                for (int v2 = 0; v2 < 2; ++v2) {
-                    const int uu = gt + 128 * v2, rq = uu % nq, kq = uu / nq;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int k = k0 + kq * 4 + j;
-                        b[4 * v2 + j] = ld4(kq < kKQ && rq * 4 < N && k < klim ? op.b_ptr(rq * 4, k) : nullptr);
-                    }
+                for (int j = 0; j < 8; ++j) {
+                    const int uu = gt + j * 128, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
+                    const bool ok = kq < kKQ && r < N;
+                    b[j].x = ok && k < klim ? __ldg(op.b_ptr(r, k)) : 0.0f;
+                    b[j].y = ok && k + 1 < klim ? __ldg(op.b_ptr(r, k + 1)) : 0.0f;
+                    b[j].z = ok && k + 2 < klim ? __ldg(op.b_ptr(r, k + 2)) : 0.0f;
+                    b[j].w = ok && k + 3 < klim ? __ldg(op.b_ptr(r, k + 3)) : 0.0f;
                 }
             }
             // warm L2 with the B rows of this group's chunk kDw + 1 ahead (register-path B)
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
 #endif
             // B hi/lo -> smem canonical
             if constexpr (kDbgNoBreg) {
-            } else if constexpr (!Op::B_IMAGE && Op::BMODE == 0) {
+            } else if constexpr (!Op::B_IMAGE) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int uu = gt + j * 128, r = uu % nt, kq = uu / nt;
@@ -382,29 +383,6 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         *reinterpret_cast<float4*>(bh + off) = b[j];
                         *reinterpret_cast<float4*>(bl + off) =
                             make_float4(lo_of(b[j].x), lo_of(b[j].y), lo_of(b[j].z), lo_of(b[j].w));
-                    }
-                }
-            } else if constexpr (!Op::B_IMAGE) {
-                const int nq = nt >> 2;
-#pragma unroll
-                for (int v2 = 0; v2 < 2; ++v2) {
-                    const int uu = gt + 128 * v2, rq = uu % nq, kq = uu / nq;
-                    if (kq < kKQ) {
-                        const float4* bb = b + 4 * v2;
-                        const float blk[4][4] = {{bb[0].x, bb[1].x, bb[2].x, bb[3].x},
-                                                 {bb[0].y, bb[1].y, bb[2].y, bb[3].y},
-                                                 {bb[0].z, bb[1].z, bb[2].z, bb[3].z},
-                                                 {bb[0].w, bb[1].w, bb[2].w, bb[3].w}};
-#pragma unroll
-                        for (int ii = 0; ii < 4; ++ii) {
-                            const int jj = (ii + (rq >> 1)) & 3;
-                            const int r = rq * 4 + jj;
-                            const uint32_t off = kq * lbo + (r >> 3) * 128 + (r & 7) * 16;
-                            *reinterpret_cast<float4*>(bh + off) =
-                                make_float4(blk[jj][0], blk[jj][1], blk[jj][2], blk[jj][3]);
-                            *reinterpret_cast<float4*>(bl + off) = make_float4(lo_of(blk[jj][0]), lo_of(blk[jj][1]),
-                                                                               lo_of(blk[jj][2]), lo_of(blk[jj][3]));
-                        }
                     }
                 }
             }
