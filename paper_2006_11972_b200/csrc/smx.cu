@@ -237,8 +237,8 @@ template <int L>
 void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        cnn::conv1_fwd_fast<<<dim3((mb * 1024 + 511) / 512, n), 256, 0, c->cur>>>(a);
-        launch_check(c, "conv1_fwd_fast");
+        cnn::conv1_fwd_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
+        launch_check(c, "conv1_fwd_lane");
         return;
     }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
