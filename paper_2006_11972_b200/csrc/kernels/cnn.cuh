@@ -747,99 +747,18 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
 }
 
 // ---- layer 1 in tensor-core mode: fp32 SIMT kernels ---------------------------------------
-// conv1 has K = 27 and N = 32: far too thin for 128-row tcgen05 tiles, and memory-bound anyway.
-// These kernels use plain fp32 FMA (at least as accurate as 3xTF32) in their own fixed order;
-// exact mode keeps the oracle-order kernels above.
+// conv1 has K = 27 and N = 32: far too thin for 128-row tcgen05 tiles.  These kernels use fp32
+// FMAs (at least as accurate as 3xTF32) in their own fixed order, issued as packed FFMA2 (two
+// output channels per instruction: the 3-register FFMA issues at half rate on this part, so the
+// packed form is what reaches the FMA pipe's throughput); exact mode keeps the oracle-order
+// kernels above.
 
-// Register-blocked: one thread = 4 consecutive output pixels of a row x 16 output channels (64
-// accumulators), so each shared-memory weight vector feeds 16 FMAs and each input float4 of the
-// 3 x 6 window feeds up to 3 taps x 4 pixels.  W1^T staged in shared memory ([27][32], read as
-// warp-uniform broadcasts); outputs staged in shared memory and written back as contiguous 16-B
-// stores.  grid (ceil(max_batch * 1024 / 512), groups), block 256 (512 pixels = half a sample).
-__global__ void __launch_bounds__(256) conv1_fwd_fast(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
-    __shared__ __align__(16) float wt[27][32];
-    __shared__ float bs_[32];
-    __shared__ __align__(16) float stage[256 * 36];  // 256 pixels x (32 + 4 pad) floats, two passes
-    if (blockIdx.x * 512 >= v.bs * 1024) return;
-    for (int i = threadIdx.x; i < 27 * 32; i += blockDim.x) {
-        const int co = i & 31, k = i >> 5, t = k / 3, ci = k % 3;
-        wt[k][co] = v.w[Geo<1>::OffW + (co * 9 + t) * 4 + ci];
-    }
-    if (threadIdx.x < 32) bs_[threadIdx.x] = v.w[Geo<1>::OffB + threadIdx.x];
-    __syncthreads();
-    const float* in = layer_in<1>(p, v);
-    const int hh = threadIdx.x & 1;                 // channel half: co in [16 hh, 16 hh + 16)
-    const int pq = blockIdx.x * 128 + (threadIdx.x >> 1);  // pixel quad (4 pixels of one row)
-    const int m0 = pq * 4;                           // first pixel (always < bs * 1024: 1024 % 512 == 0)
-    const int n = m0 >> 10, oh = (m0 >> 5) & 31, ow0 = m0 & 31;
-    float acc[4][16];
-#pragma unroll
-    for (int px = 0; px < 4; ++px)
-#pragma unroll
-        for (int c = 0; c < 16; ++c) acc[px][c] = bs_[16 * hh + c];
-#pragma unroll
-    for (int dh = 0; dh < 3; ++dh) {
-        const int ih = oh + dh - 1;
-        if ((unsigned)ih >= 32u) continue;
-        float4 xr[6];  // input columns ow0 - 1 .. ow0 + 4
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-            const int iw = ow0 + j - 1;
-            xr[j] = (unsigned)iw < 32u ? __ldg(reinterpret_cast<const float4*>(in + (((n << 5) + ih) * 32 + iw) * 4))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int dw = 0; dw < 3; ++dw) {
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const float4* wr = reinterpret_cast<const float4*>(&wt[(dh * 3 + dw) * 3 + ci][16 * hh]);
-                const float4 w0 = wr[0], w1 = wr[1], w2 = wr[2], w3 = wr[3];
-                const float wv[16] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w,
-                                      w2.x, w2.y, w2.z, w2.w, w3.x, w3.y, w3.z, w3.w};
-#pragma unroll
-                for (int px = 0; px < 4; ++px) {
-                    const float4 xv4 = xr[px + dw];
-                    const float xv = ci == 0 ? xv4.x : ci == 1 ? xv4.y : xv4.z;
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) acc[px][c] = __fmaf_rn(xv, wv[c], acc[px][c]);
-                }
-            }
-        }
-    }
-    // two passes of 256 pixels (threads 0-127, then 128-255) through the staging buffer
-    const int m_first = blockIdx.x * 512;
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-        __syncthreads();
-        if ((threadIdx.x >> 7) == pass) {
-#pragma unroll
-            for (int px = 0; px < 4; ++px) {
-                float4* st = reinterpret_cast<float4*>(stage + (((threadIdx.x & 127) >> 1) * 4 + px) * 36 + 16 * hh);
-#pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4)
-                    st[c4] = make_float4(fmaxf(acc[px][4 * c4], 0.0f), fmaxf(acc[px][4 * c4 + 1], 0.0f),
-                                         fmaxf(acc[px][4 * c4 + 2], 0.0f), fmaxf(acc[px][4 * c4 + 3], 0.0f));
-            }
-        }
-        __syncthreads();
-        const int base = m_first + pass * 256;
-        const int rows = min(256, v.bs * 1024 - base);
-        float4* out = reinterpret_cast<float4*>(layer_out<1>(p, v) + (long long)base * 32);
-        for (int i = threadIdx.x; i < rows * 8; i += blockDim.x)
-            out[i] = reinterpret_cast<float4*>(stage)[(i >> 3) * 9 + (i & 7)];
-    }
-}
-
-// Packed fp32 FMA (FFMA2): two accumulators += a pair of values x one broadcast scalar.  The pair
-// must be an aligned register pair (the .x/.y or .z/.w halves of a float4).
+// Packed fp32 FMA (FFMA2): a register pair of accumulators += a register pair x a scalar that
+// ptxas broadcasts to both halves (written here as the pair {x, x}).
 __device__ __forceinline__ unsigned long long f2pack(float a, float b) {
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
     return r;
-}
-__device__ __forceinline__ void ffma2(unsigned long long& acc, float x0, float x1, float w) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(f2pack(x0, x1)), "l"(f2pack(w, w)));
 }
 __device__ __forceinline__ float2 f2unpack(unsigned long long v) {
     float2 r;
@@ -938,68 +857,105 @@ __global__ void __launch_bounds__(256) conv1_fwd_lane(ConvArgs p) {
     }
 }
 
-// Per-sample partial weight gradient of conv1: block = one (sample, slot); lane = output channel,
-// 28 accumulators per lane (27 taps x channels + bias); the sample's zero-padded image is staged
-// in shared memory and read as warp-uniform broadcasts; the 8 warps' partials are combined in a
-// fixed order.  partial[n][co*28 + j].  grid (max_batch, groups), block 256.
-__global__ void __launch_bounds__(256) conv1_wgrad_fast(ConvArgs p) {
+// Per-sample partial weight gradient of conv1 with packed FMAs, the forward's structure with the
+// roles of weights and pixels swapped: thread = output-channel pair (co, co + 1) x one 8-pixel
+// segment per step; its 27 (tap, ci) accumulators (+ bias) are register pairs, and each FFMA2
+// adds the pair's two output gradients (one 8-byte load, 128 bytes per half-warp and pixel) times
+// a broadcast input value read from the planar image.  The next segment's output gradients are
+// loaded while the current one is accumulated; the 16 segment streams of a block are combined in
+// a fixed order per sample.  A block walks samples x, x + gridDim.x, ... of its slot with the next
+// image prefetched.  partial[n][co*28 + j], j = tap*3 + ci (27 = bias).  grid (min(max_batch, 32),
+// groups), block 256.
+__global__ void __launch_bounds__(256, 2) conv1_wgrad_lane(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
-    const int n = blockIdx.x;
-    if (n >= v.bs) return;
-    __shared__ __align__(16) float img[34 * 34 * 4];
+    if ((int)blockIdx.x >= v.bs) return;
+    __shared__ __align__(16) float pl[3 * kPlane];
     __shared__ float red[8][kL1Outs];
-    const float* in = layer_in<1>(p, v) + (long long)n * 4096;
-    for (int i = threadIdx.x; i < 34 * 34; i += blockDim.x) {
-        const int y = i / 34 - 1, x = i % 34 - 1;
-        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-        if ((unsigned)y < 32u && (unsigned)x < 32u) val = __ldg(reinterpret_cast<const float4*>(in + (y * 32 + x) * 4));
-        reinterpret_cast<float4*>(img)[i] = val;
-    }
+    for (int i = threadIdx.x; i < 3 * kPlane; i += blockDim.x) pl[i] = 0.0f;  // borders stay zero
+    const float* in = layer_in<1>(p, v);
+    float4 img[4];
+    auto load = [&](int n) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            img[j] = __ldg(reinterpret_cast<const float4*>(in + (long long)n * 4096 + (threadIdx.x + 256 * j) * 4));
+    };
+    auto stage = [&]() {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = threadIdx.x + 256 * j;
+            const int o = ((i >> 5) + 1) * kPlW + (i & 31) + 1;
+            pl[o] = img[j].x; pl[kPlane + o] = img[j].y; pl[2 * kPlane + o] = img[j].z;
+        }
+    };
+    load(blockIdx.x);
     __syncthreads();
-    const int warp = threadIdx.x >> 5, co = threadIdx.x & 31;
-    const float* dy = layer_dout<1>(p, v) + (long long)n * 1024 * 32;
-    float acc[28];
+    stage();
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cp = lane & 15, half = lane >> 4, co = 2 * cp;
+    const unsigned long long one = f2pack(1.0f, 1.0f);
+#pragma unroll 1
+    for (int n = blockIdx.x; n < v.bs; n += gridDim.x) {
+        const bool more = n + (int)gridDim.x < v.bs;
+        if (more) load(n + gridDim.x);
+        const float* dy = layer_dout<1>(p, v) + (long long)n * 1024 * 32 + co;
+        auto seg_px = [&](int q) { return (warp * 4 + (q >> 1)) * 32 + (q & 1) * 16 + half * 8; };
+        unsigned long long acc[28];
 #pragma unroll
-    for (int j = 0; j < 28; ++j) acc[j] = 0.0f;
-    // 4 consecutive pixels of a row per step: their 3 x 6 input window (18 broadcast float4 loads)
-    // feeds 4 x 27 FMAs per lane
-    for (int p0 = warp * 128; p0 < warp * 128 + 128; p0 += 8) {
-        float dv[8];
+        for (int j = 0; j < 28; ++j) acc[j] = 0ull;
+        unsigned long long d[8], dn[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dv[e] = __ldg(dy + (p0 + e) * 32 + co);  // 8 loads in flight
+        for (int px = 0; px < 8; ++px) d[px] = __ldg(reinterpret_cast<const unsigned long long*>(dy + (seg_px(0) + px) * 32));
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+            const int m0 = seg_px(q), oh = m0 >> 5, p0 = m0 & 31;
+            if (q + 1 < 8) {
+                const int m1 = seg_px(q + 1);
 #pragma unroll
-        for (int hq = 0; hq < 2; ++hq) {
-            const int pix0 = p0 + 4 * hq, oh = pix0 >> 5, ow0 = pix0 & 31;
-#pragma unroll
-            for (int dh = 0; dh < 3; ++dh) {
-                float4 xr[6];
-#pragma unroll
-                for (int j = 0; j < 6; ++j) xr[j] = reinterpret_cast<const float4*>(img)[(oh + dh) * 34 + ow0 + j];
-#pragma unroll
-                for (int px = 0; px < 4; ++px) {
-                    const float d = dv[4 * hq + px];
-#pragma unroll
-                    for (int dw = 0; dw < 3; ++dw) {
-                        const float4 x = xr[px + dw];
-                        const int t = dh * 3 + dw;
-                        acc[t * 3] = __fmaf_rn(d, x.x, acc[t * 3]);
-                        acc[t * 3 + 1] = __fmaf_rn(d, x.y, acc[t * 3 + 1]);
-                        acc[t * 3 + 2] = __fmaf_rn(d, x.z, acc[t * 3 + 2]);
-                    }
-                }
+                for (int px = 0; px < 8; ++px) dn[px] = __ldg(reinterpret_cast<const unsigned long long*>(dy + (m1 + px) * 32));
             }
 #pragma unroll
-            for (int px = 0; px < 4; ++px) acc[27] = __fadd_rn(acc[27], dv[4 * hq + px]);
-        }
-    }
+            for (int dh = 0; dh < 3; ++dh)
 #pragma unroll
-    for (int j = 0; j < 28; ++j) red[warp][co * 28 + j] = acc[j];
-    __syncthreads();
-    float* part = v.act + p.al.w1p + (long long)n * kL1Outs;
-    for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
-        float s_ = red[0][i];
-        for (int w = 1; w < 8; ++w) s_ = __fadd_rn(s_, red[w][i]);
-        part[i] = s_;
+                for (int ci = 0; ci < 3; ++ci) {
+                    const float* r = pl + ci * kPlane + (oh + dh) * kPlW + p0;
+                    const float4 x0 = *reinterpret_cast<const float4*>(r);
+                    const float4 x1 = *reinterpret_cast<const float4*>(r + 4);
+                    const float2 x2 = *reinterpret_cast<const float2*>(r + 8);
+                    const float x[10] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y};
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw)
+#pragma unroll
+                        for (int px = 0; px < 8; ++px)
+                            asm("fma.rn.f32x2 %0, %1, %2, %0;"
+                                : "+l"(acc[(dh * 3 + dw) * 3 + ci]) : "l"(d[px]), "l"(f2pack(x[px + dw], x[px + dw])));
+                }
+#pragma unroll
+            for (int px = 0; px < 8; ++px) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[27]) : "l"(d[px]), "l"(one));
+#pragma unroll
+            for (int px = 0; px < 8; ++px) d[px] = dn[px];
+        }
+        // half-warps hold the same channel pair: fold, then the 8 warps in order
+#pragma unroll
+        for (int j = 0; j < 28; ++j) {
+            float2 a = f2unpack(acc[j]);
+            a.x = __fadd_rn(a.x, __shfl_xor_sync(0xffffffffu, a.x, 16));
+            a.y = __fadd_rn(a.y, __shfl_xor_sync(0xffffffffu, a.y, 16));
+            if (half == 0) {
+                red[warp][co * 28 + j] = a.x;
+                red[warp][(co + 1) * 28 + j] = a.y;
+            }
+        }
+        __syncthreads();
+        float* part = v.act + p.al.w1p + (long long)n * kL1Outs;
+        for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
+            float s_ = red[0][i];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) s_ = __fadd_rn(s_, red[w][i]);
+            part[i] = s_;
+        }
+        if (more) stage();
+        __syncthreads();  // planes and red reused by the next sample
     }
 }
 

@@ -254,8 +254,8 @@ template <int L>
 void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        cnn::conv1_wgrad_fast<<<dim3(mb, n), 256, 0, c->cur>>>(a);
-        launch_check(c, "conv1_wgrad_fast");
+        cnn::conv1_wgrad_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
+        launch_check(c, "conv1_wgrad_lane");
         cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a);
         launch_check(c, "conv1_wgrad_reduce");
         return;
