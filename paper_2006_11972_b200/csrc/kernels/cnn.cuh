@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
     const int c = threadIdx.x;
     const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
     float s = 0.0f;
-    for (int pix = 0; pix < 64; ++pix) s = __fadd_rn(s, a3[pix * kFeat + c]);
+#pragma unroll 16
+    for (int pix = 0; pix < 64; ++pix) s = __fadd_rn(s, __ldg(a3 + pix * kFeat + c));  // loads run ahead
     g[c] = __fmul_rn(s, 0.015625f);
     if (!p.zout) v.act[p.al.g + (long long)n * kFeat + c] = g[c];
     __syncthreads();
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(128) head_dg_kernel(ConvArgs p) {
     const float dg = __fmul_rn(acc, 0.015625f);
     const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
     float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
-    for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = a3[pix * kFeat + c] > 0.0f ? dg : 0.0f;
+#pragma unroll 16
+    for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
 }
 
 // ---- tensor-core mode: implicit-GEMM Op policies for conv_ws.cuh ---------------------------
