@@ -474,6 +474,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         // this warp's accumulator columns: half of the tile (all of it below 32 columns)
         const bool halves = Plan::EpiWarps == 8 && nt >= 32;
         const int cw = halves ? nt / 2 : (ch == 0 ? nt : 0), cbeg = halves ? ch * cw : 0;
+        constexpr int kCW = Plan::EpiWarps == 8 ? Plan::N / 2 : Plan::N;  // most columns a warp drains
+        // (register sums only where the register budget allows: the 13-warp kernels)
+        constexpr bool kRegSum = Plan::EpiWarps == 4 && kCW <= 64 && kCW % 16 == 0;
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
@@ -483,37 +486,84 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 if (m < M)
                     for (int col = 32 * ch; col < N; col += 32 * (Plan::EpiWarps / 4)) prefetch_l2(op.mask_at(m, col));
             }
-            // sum the tile's segments into sacc (round-to-nearest fp32 adds, fixed order)
-            for (int j = 0; j < nseg; ++j, ++un) {
-                const int acc_i = un & 1, use = un >> 1;
-                mbar_wait(&accf[acc_i], use & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                if (cw == 0) {  // nothing to drain for this warp: release at once
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&acce[acc_i]);
-                }
-                for (int c0 = cbeg; c0 < cbeg + cw; c0 += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;");
-                    if (c0 + 16 >= cbeg + cw) {
+            // sum the tile's segments (round-to-nearest fp32 adds, fixed order): in registers when
+            // a warp drains at most 64 columns, then once into sacc; otherwise in sacc directly
+            if constexpr (kRegSum) {
+                float sum[kCW];
+                for (int j = 0; j < nseg; ++j, ++un) {
+                    const int acc_i = un & 1, use = un >> 1;
+                    mbar_wait(&accf[acc_i], use & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (cw == 0) {
                         asm volatile("tcgen05.fence::before_thread_sync;");
                         mbar_arrive(&acce[acc_i]);
                     }
 #pragma unroll
-                    for (int jj = 0; jj < 16; jj += 4) {
-                        float4* sp = s4(row, (c0 + jj) >> 2);
-                        const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
-                                                      __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
-                        if (j == 0) {
-                            *sp = nv;
-                        } else {
-                            float4 o = *sp;
-                            o.x = __fadd_rn(o.x, nv.x);
-                            o.y = __fadd_rn(o.y, nv.y);
-                            o.z = __fadd_rn(o.z, nv.z);
-                            o.w = __fadd_rn(o.w, nv.w);
-                            *sp = o;
+                    for (int b16 = 0; b16 < kCW / 16; ++b16) {
+                        if (16 * b16 < cw) {
+                            uint32_t r[16];
+                            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + cbeg + 16 * b16, r);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;");
+                            if (16 * b16 + 16 >= cw) {
+                                asm volatile("tcgen05.fence::before_thread_sync;");
+                                mbar_arrive(&acce[acc_i]);
+                            }
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj)
+                                sum[16 * b16 + jj] = j == 0 ? __uint_as_float(r[jj]) : __fadd_rn(sum[16 * b16 + jj], __uint_as_float(r[jj]));
+                        }
+                    }
+                }
+                if constexpr (Op::EPI == ctc::kEpiPartT) {
+#ifndef SMX_DBG_NO_EPI
+                    // transposed outputs straight from registers: lanes = consecutive rows of one
+                    // column (coalesced)
+                    const int m = mt0 + row;
+                    if (m < M) {
+#pragma unroll
+                        for (int cc = 0; cc < kCW; ++cc)
+                            if (cc < cw && cbeg + cc < N) *op.ct_at(cbeg + cc, m) = sum[cc];
+                    }
+#endif
+                    continue;
+                } else {
+#pragma unroll
+                    for (int c4 = 0; c4 < kCW / 4; ++c4)
+                        if (4 * c4 < cw)
+                            *s4(row, (cbeg >> 2) + c4) = make_float4(sum[4 * c4], sum[4 * c4 + 1], sum[4 * c4 + 2], sum[4 * c4 + 3]);
+                }
+            } else {
+                for (int j = 0; j < nseg; ++j, ++un) {
+                    const int acc_i = un & 1, use = un >> 1;
+                    mbar_wait(&accf[acc_i], use & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (cw == 0) {  // nothing to drain for this warp: release at once
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        mbar_arrive(&acce[acc_i]);
+                    }
+                    for (int c0 = cbeg; c0 < cbeg + cw; c0 += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;");
+                        if (c0 + 16 >= cbeg + cw) {
+                            asm volatile("tcgen05.fence::before_thread_sync;");
+                            mbar_arrive(&acce[acc_i]);
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < 16; jj += 4) {
+                            float4* sp = s4(row, (c0 + jj) >> 2);
+                            const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
+                                                          __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
+                            if (j == 0) {
+                                *sp = nv;
+                            } else {
+                                float4 o = *sp;
+                                o.x = __fadd_rn(o.x, nv.x);
+                                o.y = __fadd_rn(o.y, nv.y);
+                                o.z = __fadd_rn(o.z, nv.z);
+                                o.w = __fadd_rn(o.w, nv.w);
+                                *sp = o;
+                            }
                         }
                     }
                 }
@@ -524,13 +574,19 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 // consecutive 16 bytes of a row
                 asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // the whole tile is in sacc
                 const int q4 = N / 4;
+                // the thread's column quad is fixed when the stride is a multiple of the row
+                // length: its bias quad is then loaded once per tile
+                const bool fixed_c4 = Plan::EpiThreads % q4 == 0;
+                float4 bfix = make_float4(0.f, 0.f, 0.f, 0.f);
+                if constexpr (Op::EPI != ctc::kEpiStore)
+                    if (fixed_c4) bfix = op.bias4(4 * (et % q4));
                 for (int e = et; e < kBM * q4; e += Plan::EpiThreads) {
                     const int r = e / q4, c4 = e % q4, m = mt0 + r;
                     if (m >= M) continue;
                     if (4 * c4 >= N) continue;
                     float4 x = *s4(r, c4);
                     if constexpr (Op::EPI != ctc::kEpiStore) {
-                        const float4 b = op.bias4(4 * c4);
+                        const float4 b = fixed_c4 ? bfix : op.bias4(4 * c4);
                         x.x = __fadd_rn(x.x, b.x); x.y = __fadd_rn(x.y, b.y);
                         x.z = __fadd_rn(x.z, b.z); x.w = __fadd_rn(x.w, b.w);
                     }
