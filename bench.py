@@ -38,6 +38,8 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 TRAFFIC: dict = {
     # profiles/r01/ncu_conv2_fwd_full.txt: 64 groups at bs 128 (= the bench's roofline launch)
     "conv_ws_kernel<Fwd<2>>": 1_083_516_000 + 506_999_552,
+    # profiles/r01/ncu_ws_full.txt: conv2 weight-gradient GEMM, 64 groups at bs 128
+    "conv_ws_kernel<Wgrad<2>>": 1_674_893_000 + 75_405_000,
 }
 METRIC = "trial-equivalent train steps/sec per study"
 UNIT = "trial-steps/s"
@@ -396,7 +398,8 @@ def main():
     P = kx.p_algo
     kx.close()
     upd_bytes, fork_bytes = 20 * P * n_h, 16 * P * n_h
-    if cnn:  # conv2: M = 128 x 16 x 16 output pixels, N = 64, K = 9 x 32 (both kinds)
+    if cnn:  # conv2: M = 128 x 16 x 16 output pixels, N = 64, K = 9 x 32 (forward; the weight
+        # gradient is the same product count with M and K exchanged)
         gemm_flops = 2 * 128 * 256 * 288 * 64 * n_k
     else:  # layer 1: 128 x 256 x 784 (both kinds)
         gemm_flops = 2 * 128 * 256 * 784 * n_k
@@ -421,9 +424,11 @@ def main():
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
-        roofline = dict(kernels["K1_conv2_fwd"])
-        roofline["kernel"] = ("conv_ws_kernel<Fwd<2>> (conv2 implicit GEMM, 64 groups x M 32768 x N 64 x K 288)"
-                              if gemm_mode == ex.GEMM_TC else "conv_fwd_simt<2>")
+        # the largest single kernel of a lockstep (profiles/r01/launches_bench_c2.txt): the conv2
+        # weight gradient, M 288 (tap, cin) x N 64 (cout) x K 32768 (sample, pixel) per group
+        roofline = dict(kernels["K3_conv2_wgrad"])
+        roofline["kernel"] = ("conv_ws_kernel<Wgrad<2>> (conv2 weight-gradient implicit GEMM, 64 groups x M 288 x "
+                              "N 64 x K 32768, split 16 ways)" if gemm_mode == ex.GEMM_TC else "conv_wgrad_simt<2>")
     else:
         kernels = {
             "K1_fwd1_gemm": tensor("fwd1", gemm_flops, ms[2]),

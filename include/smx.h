@@ -150,8 +150,8 @@ int smx_reset_stats(smx_ctx* ctx);
 /* Standalone launches of one kernel class for roofline measurement: kind 0 = K5 update over
  * `n` slots, 1 = K6 fork copy of `n` checkpoints, 2 = the layer-1 forward GEMM over `n` slots,
  * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size);
- * for the CNN, 2 = the conv2 forward implicit GEMM and 3 = the conv2 weight gradient (split GEMM +
- * ordered reduction).
+ * for the CNN, 2 = the conv2 forward implicit GEMM and 3 = the conv2 weight-gradient implicit
+ * GEMM (tensor-core mode: the split GEMM alone; exact mode: the SIMT kernel).
  * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
 

@@ -1135,10 +1135,15 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             c->cur = c->stream;
             weight_images(c, a, n);
             auto launch = [&] {
-                if (kind == 2)
+                if (kind == 2) {
                     conv_forward<2>(c, a, n, c->d.max_batch);
-                else
+                } else if (c->d.gemm_mode == SMX_GEMM_TC) {  // the implicit GEMM alone (no split reduction)
+                    using G = cnn::Geo<2>;
+                    const int splits = (c->d.max_batch * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
+                    conv_tc<cnn::ctc::Wgrad<2>>(c, a, splits, cnn::Part<2>::Rows, n);
+                } else {
                     conv_wgrad<2>(c, a, n, c->d.max_batch);
+                }
             };
             for (int w = 0; w < 3; ++w) launch();
             cudaEventRecord(c->ev[6], c->stream);
