@@ -12,6 +12,8 @@
 // all-ones row of the im2col operand.  conv1 (K = 27) uses fp32 SIMT kernels in both modes.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded on the host through the runtime's driver entry point)
+
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "step_kernels.cuh"
@@ -129,6 +131,12 @@ inline ActLayout act_layout(int max_batch) {
     return L;
 }
 
+// TMA tensor maps of the tensor-core convolutions' A operands, per slot (NHWC fp32, dims
+// innermost first: channel, column, row, sample = max_batch; 128-byte swizzle; zero fill out of
+// bounds): the conv2 / conv3 forward inputs (a1 / a2, loaded with a column and row traversal
+// stride of 2) and the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients.
+enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmapKinds = 4 };
+
 struct ConvArgs {
     const int* slots;
     const SlotState* st;
@@ -146,6 +154,7 @@ struct ConvArgs {
     float* grad;
     long long grad_stride;
     const int* labels;   // training labels (slot offset) or validation labels (x_row0)
+    const CUtensorMap* tmaps;  // [slot][kTmapKinds]: TMA maps of the implicit-GEMM A operands
     float* loss_hist;
     float* zout;         // eval: logits [group][n_val][16]
     long long z_stride;
@@ -464,7 +473,10 @@ struct Fwd {
     using G = Geo<L>;
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
+    static constexpr bool A_TMA = (L >= 2);  // A tile = one strided TMA box per chunk
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = L == 3 ? 8 : 4;
+    static constexpr int kRowsPerSample = G::OH * G::OH;
+    const CUtensorMap* tmap;
     const float* in;
     const float* w;
     const float* bias;
@@ -483,6 +495,7 @@ struct Fwd {
     __device__ void setup(const ConvArgs& p, int z, int tile_y) {
         const SlotView v = slot_view(p, p.slots[z]);
         img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
+        tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmFwd3 : kTmFwd2);
         in = layer_in<L>(p, v);
         w = v.w + G::OffW;
         bias = v.w + G::OffB;
@@ -523,6 +536,16 @@ struct Fwd {
         return (r.vmask >> t.bit) & 1u ? r.ptr + t.off : nullptr;
     }
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
+    // TMA box origin (channel, column, row, sample) of M tile `tile`, reduction chunk k0: output
+    // rows (n, oh, ow) -> input (2 oh + kh - 1, 2 ow + kw - 1), one tap and 32 channels per chunk
+    __device__ __forceinline__ void a_coords(int tile, int k0, int* c) const {
+        const int m0 = tile * kBM, t = k0 / G::Ci;
+        const int n = m0 / kRowsPerSample, oh0 = (m0 % kRowsPerSample) / G::OH;
+        c[0] = k0 % G::Ci;
+        c[1] = t % 3 - 1;
+        c[2] = G::S * oh0 + t / 3 - 1;
+        c[3] = n;
+    }
     __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
     __device__ __forceinline__ float* c_row(int m) const { return out + (long long)m * G::Co; }
     __device__ __forceinline__ float* c_at(int m, int col) const { return out + (long long)m * G::Co + col; }
@@ -544,8 +567,10 @@ struct Dgrad {
     static_assert(G::S == 2, "sub-pixel decomposition is for stride 2");
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
+    static constexpr bool A_TMA = true;  // A tile = one shifted TMA box of dy per chunk
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
+    const CUtensorMap* tmap;
     const float* dy;
     const float* w;
     const float* act;
@@ -561,6 +586,7 @@ struct Dgrad {
     __device__ void setup(const ConvArgs& p, int z, int half) {
         const SlotView v = slot_view(p, p.slots[z]);
         dy = layer_dout<L>(p, v);
+        tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 2 ? kTmDgr2 : kTmDgr3);
         w = v.w + G::OffW;
         act = layer_out<L - 1>(p, v);
         dx = layer_dout<L - 1>(p, v);
@@ -591,6 +617,15 @@ struct Dgrad {
         return (r.vmask >> t.bit) & 1u ? r.ptr + t.off : nullptr;
     }
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
+    // TMA box origin (channel, column, row, sample): rows (n, a, b) of M tile `tile` read dy at
+    // (a + da, b + db), channels co0 .. co0 + 31 of chunk k0 = (neighbour, co0)
+    __device__ __forceinline__ void a_coords(int tile, int k0, int* c) const {
+        const int m0 = tile * kBM, nb = k0 / G::Co;
+        c[0] = k0 % G::Co;
+        c[1] = nb & 1;
+        c[2] = (m0 % (HH * HH)) / HH + (nb >> 1);
+        c[3] = m0 / (HH * HH);
+    }
     // epilogue column c (0..N-1) -> (class, ci); rows write 4 input pixels
     __device__ __forceinline__ long long pix_off(int r, int col) const {
         const int cc = col0 + col, cls = cc / G::Ci;
@@ -616,7 +651,7 @@ template <int L>
 struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
-    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = false;
     struct RowInfo {
         int kh, kw, ci;  // tap and first channel of a row quad (kh = -1000: padding rows)
     };

@@ -50,14 +50,14 @@ struct WsPlan {
     static constexpr int BStage = N * 256;                          // hi + lo tiles
     static constexpr int Sacc = kBM * N * 4;                        // tile sums [row][N], 16-B units
                                                                     // XOR-swizzled by row
-    static constexpr int Fixed = Stages * BStage + 128 + Sacc;
+    static constexpr int Fixed = Stages * BStage + 256 + Sacc;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
     // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
     static constexpr int ARaw = (ARawMax > 8 ? 8 : ARawMax) & ~1;
     static_assert(ARaw >= 4, "shared memory plan");
     static constexpr int ARawOff = Stages * BStage;
     static constexpr int BarOff = ARawOff + ARaw * kARawTile;
-    static constexpr int SaccOff = BarOff + 128;
+    static constexpr int SaccOff = BarOff + 256;
     static constexpr int Bytes = SaccOff + Sacc;
     // epilogue: one warp per TMEM lane quadrant (4), or two each draining half the columns (8)
     static constexpr int EpiWarps = Op::kEpiWarps;
@@ -145,6 +145,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // two instructions per element instead of rna/sub/rna.
 __device__ __forceinline__ float lo_of(float a) { return __fsub_rn(a, __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
 
+#ifdef SMX_DBG_TIMELINE
+// profiling variant: clock64 timeline of one CTA ((0, 1, 1)) of the first launch after the host
+// arms it (smx_dbg_timeline): producer lanes 0 of warps 0 / 4 per chunk [0, 1024), MMA lane per
+// chunk [1024, 1536), epilogue warp 0 lane 0 per segment / tile [2048, 4096)
+__device__ unsigned long long smx_tl[4096];
+__device__ int smx_tl_armed;
+#define SMX_TL(i, cond) do { if (tl_on && (cond) && (i) < 4096) smx_tl[(i)] = clock64(); } while (0)
+#else
+#define SMX_TL(i, cond) do { } while (0)
+#endif
+
 template <class Op>
 __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typename Op::Args p, int tiles) {
     extern __shared__ __align__(1024) char smem[];
@@ -155,7 +166,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
     uint64_t* empty = full + kStages;
     uint64_t* accf = empty + kStages;
     uint64_t* acce = accf + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+    uint64_t* rawf = acce + 2;  // TMA A operands: raw slot filled (expect_tx) / released by the group's 4 warps
+    uint64_t* rawe = rawf + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawe + 8);
 
     Op op;
     op.setup(p, blockIdx.z, blockIdx.x);
@@ -186,12 +199,25 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             mbar_init(&accf[a], 1);
             mbar_init(&acce[a], Plan::EpiThreads);
         }
+        if constexpr (Op::A_TMA)
+            for (int r = 0; r < kARaw; ++r) {
+                mbar_init(&rawf[r], 1);
+                mbar_init(&rawe[r], 4);
+            }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+#ifdef SMX_DBG_TIMELINE
+    __shared__ int tl_flag;
+    if (threadIdx.x == 0)
+        tl_flag = (blockIdx.x == 0 && blockIdx.y == 1 && blockIdx.z == 1) ? atomicExch(&smx_tl_armed, 0) : 0;
+    __syncthreads();
+    const bool tl_on = tl_flag != 0;
+    if (tl_on && threadIdx.x == 0) smx_tl[4095] = clock64();
+#endif
 
     if (warp < kEpiWarp0) {
         // ================= producers =================
@@ -209,7 +235,24 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             if (pf_g < total) {
                 const int mm0 = (tile0 + pf_tile) * kBM, kk0 = op.kbeg + pf_chunk * kKC;
                 const uint32_t dst = araw + pf_slot * kARawTile;
-                if constexpr (Op::AM == 0) {
+                if constexpr (Op::A_TMA) {
+                    // one TMA box per chunk (128 rows x 32 k, 128-byte swizzle = the XOR layout the
+                    // rows are read with), issued by the group's first lane once the group has
+                    // released the slot's previous chunk
+                    if (q == 0 && lane == 0) {
+                        const int use = ((pf_g - grp) >> 1) / (kARaw / 2);
+                        if (use > 0) mbar_wait(&rawe[pf_slot], (use - 1) & 1);
+                        int c[4];
+                        op.a_coords(tile0 + pf_tile, kk0, c);
+                        const uint32_t bar = smem_u32(&rawf[pf_slot]);
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kARawTile));
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+                            "l"(op.tmap), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(bar)
+                            : "memory");
+                    }
+                } else if constexpr (Op::AM == 0) {
                     // unit j: row 32q + lane/8 + 4j, k-quad lane%8 (8 lanes = one row's 128 bytes)
                     if (pf_tile != ri_tile) {
 #pragma unroll
@@ -248,7 +291,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     }
                 }
             }
-            asm volatile("cp.async.commit_group;");
+            if constexpr (!Op::A_TMA) asm volatile("cp.async.commit_group;");
             pf_g += 2;
             pf_chunk += 2;
             while (pf_chunk >= nchunks) { pf_chunk -= nchunks; ++pf_tile; }
@@ -276,6 +319,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         while (c >= nchunks) { c -= nchunks; ++i; }
         for (int g = grp; g < total; g += 2) {
             const int s = g % kStages, u = g / kStages;
+            SMX_TL(g * 8 + 0, gt == 0);
             const int m = (tile0 + i) * kBM + q * 32 + lane;
             const int k0 = op.kbeg + c * kKC;
             // B (register path, non-image Ops): the group's 128 threads cover the tile
@@ -319,11 +363,14 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 }
             }
             float a[32];
-            if constexpr (kDw > 1)
+            if constexpr (Op::A_TMA)
+                mbar_wait(&rawf[rd_slot], ((((g - grp) >> 1) / (kARaw / 2)) & 1));
+            else if constexpr (kDw > 1)
                 asm volatile("cp.async.wait_group %0;" ::"n"(kDw - 1) : "memory");  // own copies of chunk g
             else
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
+            SMX_TL(g * 8 + 1, gt == 0);
             {
                 const char* rawg = smem + Plan::ARawOff + rd_slot * kARawTile;
                 const int r = q * 32 + lane;
@@ -340,6 +387,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 }
             }
             __syncwarp();  // this warp's reads of the slot precede the refill below
+            if constexpr (Op::A_TMA)
+                if (lane == 0) mbar_arrive(&rawe[rd_slot]);
+            SMX_TL(g * 8 + 5, gt == 0);
             a_issue();
             rd_slot += 2;
             if (rd_slot >= kARaw) rd_slot -= kARaw;
@@ -348,7 +398,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 for (int j = 0; j < 32; ++j) a[j] = k0 + j < klim ? 1.0f : 0.0f;
             }
             // ---- wait until the MMAs of this stage's previous use are done
+            SMX_TL(g * 8 + 2, gt == 0);
             if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+            SMX_TL(g * 8 + 3, gt == 0);
             char* bh = smem + s * kBStage;
             char* bl = bh + nt * 128;
             if constexpr (Op::B_IMAGE) {
@@ -386,6 +438,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     }
                 }
             }
+            SMX_TL(g * 8 + 6, gt == 0);
+            asm volatile("tcgen05.wait::st.sync.aligned;");
+            SMX_TL(g * 8 + 4, gt == 0);
             asm volatile("tcgen05.wait::st.sync.aligned;");
             asm volatile("fence.proxy.async.shared::cta;");
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -415,7 +470,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         dacc = tmem + acc_i * kAcc;
                     }
                     const int s = g % kStages, u = g / kStages;
+                    SMX_TL(1024 + g * 4 + 0, lane == 0);
                     mbar_wait(&full[s], u & 1);
+                    SMX_TL(1024 + g * 4 + 1, lane == 0);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
                     const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
@@ -452,6 +509,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         }
                     }
 #endif
+                    SMX_TL(1024 + g * 4 + 2, lane == 0);
                     mma_commit_e(&empty[s]);
                     if (unit_end) {
                         mma_commit_e(&accf[acc_i]);
@@ -492,7 +550,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 float sum[kCW];
                 for (int j = 0; j < nseg; ++j, ++un) {
                     const int acc_i = un & 1, use = un >> 1;
+                    SMX_TL(2048 + un * 4 + 0, et == 0);
                     mbar_wait(&accf[acc_i], use & 1);
+                    SMX_TL(2048 + un * 4 + 1, et == 0);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     if (cw == 0) {
                         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -535,7 +595,9 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             } else {
                 for (int j = 0; j < nseg; ++j, ++un) {
                     const int acc_i = un & 1, use = un >> 1;
+                    SMX_TL(2048 + un * 4 + 0, et == 0);
                     mbar_wait(&accf[acc_i], use & 1);
+                    SMX_TL(2048 + un * 4 + 1, et == 0);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     if (cw == 0) {  // nothing to drain for this warp: release at once
                         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -568,6 +630,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     }
                 }
             }
+            SMX_TL(3072 + i * 2 + 0, et == 0);
 #ifndef SMX_DBG_NO_EPI
             if constexpr (Op::EPI == ctc::kEpiBiasRelu || Op::EPI == ctc::kEpiBias || Op::EPI == ctc::kEpiStore) {
                 // row-major output tile: cooperative, coalesced write-out, consecutive threads =
@@ -596,6 +659,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     op.store4(m, 4 * c4, x);
                 }
                 asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // sacc free for the next tile
+                SMX_TL(3072 + i * 2 + 1, et == 0);
             } else if constexpr (Op::EPI == ctc::kEpiPartT) {
                 // transposed outputs: lanes = consecutive rows of one column (coalesced)
                 const int m = mt0 + row;
@@ -629,12 +693,16 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     }
                 }
                 asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // sacc free for the next tile
+                SMX_TL(3072 + i * 2 + 1, et == 0);
             }
 #endif
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+#ifdef SMX_DBG_TIMELINE
+    if (tl_on && threadIdx.x == 0) smx_tl[4094] = clock64();
+#endif
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kWsTmemCols));
 }
 

@@ -23,7 +23,7 @@ template <int AM_, int BM_, int EPI_, bool AX, bool BX>
 struct DenseOp {
     using Args = GemmArgs;
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
-    static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false;
+    static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;
     const float* A;
     const float* B;

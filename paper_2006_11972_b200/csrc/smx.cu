@@ -6,6 +6,7 @@
 // per kernel class (grouped over slots); smx_train replays the lockstep sequence through a
 // CUDA graph keyed by the active slot set.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (through cudaGetDriverEntryPoint: no -lcuda)
 
 #include <algorithm>
 #include <cmath>
@@ -95,6 +96,7 @@ struct smx_ctx {
     cnn::ActLayout al{};
     int lockstep_launches = 14;      // kernels per captured lockstep
     float* zval = nullptr;           // CNN eval logits [kEvalChunk][n_val][16]
+    CUtensorMap* tmaps = nullptr;    // CNN: [S][cnn::kTmapKinds] TMA maps of the conv A operands
 
     long long slab_stride() const { return 2 * palloc; }
 };
@@ -178,6 +180,46 @@ void colsum(smx_ctx* c, const StepCtx& sc, int groups, long long dy_off, int ld,
 }
 
 // ---- CNN (SMX_MODEL_CNN) -------------------------------------------------------------
+// TMA maps of the tensor-core convolutions' A operands (cnn.cuh kTm*), one set per slot: NHWC
+// fp32 tensors of max_batch samples, dims innermost first (channel, column, row, sample), boxes of
+// 4096 floats (16 KB = one raw A tile), 128-byte swizzle, zero fill out of bounds.
+void make_conv_tmaps(smx_ctx* c) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q),
+       "cuTensorMapEncodeTiled entry point");
+    if (!enc || q != cudaDriverEntryPointSuccess) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled unavailable");
+    struct Spec {
+        long long off;
+        int C, W, H, n_box, w_box, h_box, stride;  // box: 32 channels x w_box x h_box x n_box samples
+    };
+    const long long mb = c->d.max_batch;
+    const Spec specs[cnn::kTmapKinds] = {
+        {c->al.a1, 32, 32, 32, 1, 16, 8, 2},   // conv2 forward: a1, output tile = 8 rows x 16 columns
+        {c->al.a2, 64, 16, 16, 2, 8, 8, 2},    // conv3 forward: a2, 2 samples x 8 x 8
+        {c->al.d2, 64, 16, 16, 1, 16, 8, 1},   // conv2 input gradient: d2, 8 x 16 blocks
+        {c->al.d3, 128, 8, 8, 2, 8, 8, 1},     // conv3 input gradient: d3, 2 samples x 8 x 8 blocks
+    };
+    std::vector<CUtensorMap> h((size_t)c->S * cnn::kTmapKinds);
+    for (int s = 0; s < c->S; ++s)
+        for (int k = 0; k < cnn::kTmapKinds; ++k) {
+            const Spec& sp = specs[k];
+            float* base = c->act + c->act_stride * s + sp.off;
+            const cuuint64_t dims[4] = {(cuuint64_t)sp.C, (cuuint64_t)sp.W, (cuuint64_t)sp.H, (cuuint64_t)mb};
+            const cuuint64_t strides[3] = {(cuuint64_t)sp.C * 4, (cuuint64_t)sp.W * sp.C * 4,
+                                           (cuuint64_t)sp.H * sp.W * sp.C * 4};
+            const cuuint32_t box[4] = {32, (cuuint32_t)(sp.w_box * sp.stride), (cuuint32_t)(sp.h_box * sp.stride),
+                                       (cuuint32_t)sp.n_box};
+            const cuuint32_t es[4] = {1, (cuuint32_t)sp.stride, (cuuint32_t)sp.stride, 1};
+            const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims,
+                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        }
+    ck(cudaMalloc(&c->tmaps, sizeof(CUtensorMap) * h.size()), "tensor maps");
+    ck(cudaMemcpy(c->tmaps, h.data(), sizeof(CUtensorMap) * h.size(), cudaMemcpyHostToDevice), "tensor maps H2D");
+}
+
 cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
     cnn::ConvArgs a{};
     a.slots = d_slots;
@@ -195,6 +237,7 @@ cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
     a.grad_stride = c->palloc;
     a.labels = c->ytrain;
     a.loss_hist = c->loss;
+    a.tmaps = c->tmaps;
     return a;
 }
 
@@ -685,6 +728,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             ck(cudaMemsetAsync(c->st, 0, sizeof(SlotState) * n_slots, c->stream), "state zero");
             for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
             c->ck_valid.assign(n_ckpts, 0);
+            if (c->cnn) make_conv_tmaps(c);
             gen_dataset(c);
             ck(cudaStreamSynchronize(c->stream), "open sync");
         } catch (...) {
@@ -702,7 +746,7 @@ int smx_close(smx_ctx* c) {
     free_graphs(c);
     void* bufs[] = {c->slab, c->grad, c->pool, c->st, c->ck_st, c->hp, c->loss, c->act, c->xtrain, c->ytrain,
                     c->xval, c->yval, c->eval_act, c->zval, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
-                    c->scratch_slots};
+                    c->scratch_slots, c->tmaps};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& e : c->ev)
@@ -1239,3 +1283,19 @@ int smx_test_gemm(smx_ctx* c, int am, int bm, int M, int N, int K, const float* 
 }
 
 }  // extern "C"
+
+#ifdef SMX_DBG_TIMELINE
+// profiling variant only: arm (arm = 1: clear and arm for the next conv_ws launch) or read the
+// clock64 timeline of conv_ws.cuh (arm = 0: copy n <= 4096 entries to out)
+extern "C" int smx_dbg_timeline(int arm, unsigned long long* out, int n) {
+    if (arm) {
+        static unsigned long long zero[4096];
+        const int one = 1;
+        if (cudaMemcpyToSymbol(smx::cnn::ws::smx_tl, zero, sizeof(zero)) != cudaSuccess) return -1;
+        if (cudaMemcpyToSymbol(smx::cnn::ws::smx_tl_armed, &one, sizeof(int)) != cudaSuccess) return -1;
+        return 0;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    return cudaMemcpyFromSymbol(out, smx::cnn::ws::smx_tl, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
+}
+#endif
