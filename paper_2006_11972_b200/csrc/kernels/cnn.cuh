@@ -134,8 +134,10 @@ inline ActLayout act_layout(int max_batch) {
 // TMA tensor maps of the tensor-core convolutions' A operands, per slot (NHWC fp32, dims
 // innermost first: channel, column, row, sample = max_batch; 128-byte swizzle; zero fill out of
 // bounds): the conv2 / conv3 forward inputs (a1 / a2, loaded with a column and row traversal
-// stride of 2) and the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients.
-enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmapKinds = 4 };
+// stride of 2), the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients, and
+// the weight gradients' im2col operands (a1 / a2 again, one box of 32 output pixels x all input
+// channels per tap).
+enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmapKinds = 6 };
 
 struct ConvArgs {
     const int* slots;
@@ -538,7 +540,9 @@ struct Fwd {
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     // TMA box origin (channel, column, row, sample) of M tile `tile`, reduction chunk k0: output
     // rows (n, oh, ow) -> input (2 oh + kh - 1, 2 ow + kw - 1), one tap and 32 channels per chunk
-    __device__ __forceinline__ void a_coords(int tile, int k0, int* c) const {
+    static constexpr int kBoxes = 1;
+    __device__ __forceinline__ int a_nbox(int) const { return 1; }
+    __device__ __forceinline__ void a_coords(int tile, int k0, int, int* c) const {
         const int m0 = tile * kBM, t = k0 / G::Ci;
         const int n = m0 / kRowsPerSample, oh0 = (m0 % kRowsPerSample) / G::OH;
         c[0] = k0 % G::Ci;
@@ -619,7 +623,9 @@ struct Dgrad {
     __device__ __forceinline__ const float* b_image(int c) const { return img + (long long)c * N * 64; }
     // TMA box origin (channel, column, row, sample): rows (n, a, b) of M tile `tile` read dy at
     // (a + da, b + db), channels co0 .. co0 + 31 of chunk k0 = (neighbour, co0)
-    __device__ __forceinline__ void a_coords(int tile, int k0, int* c) const {
+    static constexpr int kBoxes = 1;
+    __device__ __forceinline__ int a_nbox(int) const { return 1; }
+    __device__ __forceinline__ void a_coords(int tile, int k0, int, int* c) const {
         const int m0 = tile * kBM, nb = k0 / G::Co;
         c[0] = k0 % G::Co;
         c[1] = nb & 1;
@@ -651,7 +657,23 @@ template <int L>
 struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
-    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = false;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = (L >= 2);
+    // TMA: a tile's 128 rows are 128 / Ci taps x Ci channels; one box per tap = 32 output pixels
+    // (the chunk's reduction indices) x Ci channels, stored [tap][pixel][ci]
+    static constexpr int kBoxes = 128 / G::Ci, kTmaCi = G::Ci;
+    const CUtensorMap* tmap;
+    __device__ __forceinline__ int a_nbox(int tile) const {
+        const int t0 = tile * kBoxes;
+        return t0 >= 9 ? 0 : (9 - t0 < kBoxes ? 9 - t0 : kBoxes);
+    }
+    __device__ __forceinline__ void a_coords(int tile, int k0, int b, int* c) const {
+        const int t = tile * kBoxes + b;
+        const int n = k0 / (G::OH * G::OH), oh0 = (k0 % (G::OH * G::OH)) / G::OH;
+        c[0] = 0;
+        c[1] = t % 3 - 1;
+        c[2] = G::S * oh0 + t / 3 - 1;
+        c[3] = n;
+    }
     struct RowInfo {
         int kh, kw, ci;  // tap and first channel of a row quad (kh = -1000: padding rows)
     };
@@ -700,6 +722,7 @@ struct Wgrad {
         const SlotView v = slot_view(p, p.slots[z]);
         in = layer_in<L>(p, v);
         dy = layer_dout<L>(p, v);
+        tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmWg3 : kTmWg2);
         part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3);
         const int total = v.bs * G::OH * G::OH;
         split = s;

@@ -64,7 +64,10 @@ struct WsPlan {
     static_assert(EpiWarps == 4 || EpiWarps == 8, "epilogue warps");
     static constexpr int EpiThreads = EpiWarps * 32;
     static constexpr int MmaWarp = kEpiWarp0 + EpiWarps;
-    static constexpr int Threads = (MmaWarp + 1) * 32;
+    // TMA A operands: one more warp whose elected lane streams the A boxes of every chunk into the
+    // raw ring as soon as the group that read a slot has released it
+    static constexpr int TmaWarp = Op::A_TMA ? MmaWarp + 1 : -1;
+    static constexpr int Threads = (MmaWarp + (Op::A_TMA ? 2 : 1)) * 32;
 };
 template <class Op>
 constexpr int ws_smem() {
@@ -236,22 +239,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 const int mm0 = (tile0 + pf_tile) * kBM, kk0 = op.kbeg + pf_chunk * kKC;
                 const uint32_t dst = araw + pf_slot * kARawTile;
                 if constexpr (Op::A_TMA) {
-                    // one TMA box per chunk (128 rows x 32 k, 128-byte swizzle = the XOR layout the
-                    // rows are read with), issued by the group's first lane once the group has
-                    // released the slot's previous chunk
-                    if (q == 0 && lane == 0) {
-                        const int use = ((pf_g - grp) >> 1) / (kARaw / 2);
-                        if (use > 0) mbar_wait(&rawe[pf_slot], (use - 1) & 1);
-                        int c[4];
-                        op.a_coords(tile0 + pf_tile, kk0, c);
-                        const uint32_t bar = smem_u32(&rawf[pf_slot]);
-                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kARawTile));
-                        asm volatile(
-                            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-                            "l"(op.tmap), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(bar)
-                            : "memory");
-                    }
+                    // issued by the TMA warp
                 } else if constexpr (Op::AM == 0) {
                     // unit j: row 32q + lane/8 + 4j, k-quad lane%8 (8 lanes = one row's 128 bytes)
                     if (pf_tile != ri_tile) {
@@ -380,6 +368,12 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         const float4 t = *reinterpret_cast<const float4*>(rawg + r * 128 + ((kq ^ (r & 7)) << 4));
                         a[4 * kq] = t.x; a[4 * kq + 1] = t.y; a[4 * kq + 2] = t.z; a[4 * kq + 3] = t.w;
                     }
+                } else if constexpr (Op::A_TMA) {
+                    // [tap][pixel k][ci] boxes: lanes = consecutive channels (conflict-free)
+                    const float* rp = reinterpret_cast<const float*>(rawg) + (r / Op::kTmaCi) * (32 * Op::kTmaCi) +
+                                      r % Op::kTmaCi;
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) a[k] = rp[k * Op::kTmaCi];
                 } else {
                     const float* rp = reinterpret_cast<const float*>(rawg) + r;
 #pragma unroll
@@ -450,6 +444,36 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         }
 #endif
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else if (warp == Plan::TmaWarp) {
+        // ================= TMA producer of the A operands (one elected lane) =================
+        // chunk g (group g % 2) goes to raw slot g % ARaw; the slot's previous chunk g - ARaw
+        // must have been released by the 4 warps of its group
+        if constexpr (Op::A_TMA) {
+            if (lane == 0) {
+                constexpr int kBoxBytes = kARawTile / Op::kBoxes;
+                const uint32_t araw = smem_u32(smem + Plan::ARawOff);
+                int tile = 0, c = 0;
+                for (int g = 0; g < total; ++g) {
+                    const int slot = g % kARaw, use = g / kARaw;
+                    if (use > 0) mbar_wait(&rawe[slot], (use - 1) & 1);
+                    const int nbox = op.a_nbox(tile0 + tile);  // boxes past the operand are skipped
+                    const uint32_t bar = smem_u32(&rawf[slot]), dst = araw + slot * kARawTile;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                 "r"(nbox * kBoxBytes));
+                    for (int b = 0; b < nbox; ++b) {
+                        int cc[4];
+                        op.a_coords(tile0 + tile, op.kbeg + c * kKC, b, cc);
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + b * kBoxBytes),
+                            "l"(op.tmap), "r"(cc[0]), "r"(cc[1]), "r"(cc[2]), "r"(cc[3]), "r"(bar)
+                            : "memory");
+                    }
+                    if (++c == nchunks) { c = 0; ++tile; }
+                }
+            }
+            __syncwarp();
+        }
     } else if (warp == Plan::MmaWarp) {
         // ================= MMA issuer (whole warp, elected lane issues) =================
         {

@@ -24,6 +24,7 @@ struct DenseOp {
     using Args = GemmArgs;
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
     static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false;
+    static constexpr int kBoxes = 1, kTmaCi = 1;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;
     const float* A;
     const float* B;

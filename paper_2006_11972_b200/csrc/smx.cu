@@ -191,7 +191,7 @@ void make_conv_tmaps(smx_ctx* c) {
     if (!enc || q != cudaDriverEntryPointSuccess) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled unavailable");
     struct Spec {
         long long off;
-        int C, W, H, n_box, w_box, h_box, stride;  // box: 32 channels x w_box x h_box x n_box samples
+        int C, W, H, n_box, w_box, h_box, stride;  // box: 32 (conv2 / conv3 A tiles) or C channels x w_box x h_box x n_box
     };
     const long long mb = c->d.max_batch;
     const Spec specs[cnn::kTmapKinds] = {
@@ -199,6 +199,8 @@ void make_conv_tmaps(smx_ctx* c) {
         {c->al.a2, 64, 16, 16, 2, 8, 8, 2},    // conv3 forward: a2, 2 samples x 8 x 8
         {c->al.d2, 64, 16, 16, 1, 16, 8, 1},   // conv2 input gradient: d2, 8 x 16 blocks
         {c->al.d3, 128, 8, 8, 2, 8, 8, 1},     // conv3 input gradient: d3, 2 samples x 8 x 8 blocks
+        {c->al.a1, 32, 32, 32, 1, 16, 2, 2},   // conv2 weight gradient: a1, 32 output pixels (2 x 16) per tap
+        {c->al.a2, 64, 16, 16, 1, 8, 4, 2},    // conv3 weight gradient: a2, 32 output pixels (4 x 8) per tap
     };
     std::vector<CUtensorMap> h((size_t)c->S * cnn::kTmapKinds);
     for (int s = 0; s < c->S; ++s)
@@ -208,11 +210,13 @@ void make_conv_tmaps(smx_ctx* c) {
             const cuuint64_t dims[4] = {(cuuint64_t)sp.C, (cuuint64_t)sp.W, (cuuint64_t)sp.H, (cuuint64_t)mb};
             const cuuint64_t strides[3] = {(cuuint64_t)sp.C * 4, (cuuint64_t)sp.W * sp.C * 4,
                                            (cuuint64_t)sp.H * sp.W * sp.C * 4};
-            const cuuint32_t box[4] = {32, (cuuint32_t)(sp.w_box * sp.stride), (cuuint32_t)(sp.h_box * sp.stride),
-                                       (cuuint32_t)sp.n_box};
+            const bool wg = k >= cnn::kTmWg2;  // weight-gradient boxes take every channel of a tap
+            const cuuint32_t box[4] = {(cuuint32_t)(wg ? sp.C : 32), (cuuint32_t)(sp.w_box * sp.stride),
+                                       (cuuint32_t)(sp.h_box * sp.stride), (cuuint32_t)sp.n_box};
             const cuuint32_t es[4] = {1, (cuuint32_t)sp.stride, (cuuint32_t)sp.stride, 1};
             const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims,
-                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   wg ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
         }
