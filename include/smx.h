@@ -151,7 +151,8 @@ int smx_reset_stats(smx_ctx* ctx);
  * `n` slots, 1 = K6 fork copy of `n` checkpoints, 2 = the layer-1 forward GEMM over `n` slots,
  * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size);
  * for the CNN, 2 = the conv2 forward implicit GEMM and 3 = the conv2 weight-gradient implicit
- * GEMM (tensor-core mode: the split GEMM alone; exact mode: the SIMT kernel).
+ * GEMM (tensor-core mode: the split GEMM alone; exact mode: the SIMT kernel); 4 / 5 = the conv2 /
+ * conv3 input gradient, 6 = the conv3 forward, 7 = the conv3 weight gradient (with its reduction).
  * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
 

@@ -69,6 +69,7 @@ constexpr int kL1Outs = 32 * 28;
 // Per-slot activation scratch: offsets in floats, tensors [max_batch][...] (computed on host).
 struct ActLayout {
     long long a1, a2, a3, d1, d2, d3, g, z, dz, dg, rl, p1, p2, p3, wf1, wf2, wf3, wd2, wd3, w1p, stride;
+    long long mk1, mk2;  // tensor-core mode: ReLU-mask bitmaps of a1 / a2, bit e = (a[e] > 0)
 };
 
 // Tensor-core B operands that are weights are pre-split once per lockstep into "images": per K
@@ -111,6 +112,8 @@ inline ActLayout act_layout(int max_batch) {
     L.dg = take(kFeat);
     L.rl = take(1);
     L.w1p = take(kL1Outs);
+    L.mk1 = take(1024 * 32 / 32);
+    L.mk2 = take(256 * 64 / 32);
     L.p1 = o;
     o += Part<1>::Size;
     L.p2 = o;
@@ -478,6 +481,11 @@ struct Fwd {
     static constexpr bool A_TMA = (L >= 2);  // A tile = one strided TMA box per chunk
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = L == 3 ? 8 : 4;
     static constexpr int kRowsPerSample = G::OH * G::OH;
+    // the producers also record the ReLU mask of the layer input (conv2: a1, conv3: a2) as a bitmap
+    // for the input gradient of this layer: the taps (kh, kw) in {1, 2}^2 of a stride-2 conv visit
+    // every input pixel exactly once, and a producer thread holds 32 consecutive channels of it
+    static constexpr bool kInMaskBits = (L >= 2), kMaskFromBits = false;
+    uint32_t* in_bits;
     const CUtensorMap* tmap;
     const float* in;
     const float* w;
@@ -498,6 +506,7 @@ struct Fwd {
         const SlotView v = slot_view(p, p.slots[z]);
         img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
         tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmFwd3 : kTmFwd2);
+        in_bits = reinterpret_cast<uint32_t*>(v.act + (L == 3 ? p.al.mk2 : p.al.mk1));
         in = layer_in<L>(p, v);
         w = v.w + G::OffW;
         bias = v.w + G::OffB;
@@ -551,6 +560,14 @@ struct Fwd {
         c[3] = n;
     }
     __device__ __forceinline__ const float* b_ptr(int co, int k) const { return w + (long long)co * 9 * G::Ci + k; }
+    // bitmap word of row m's input pixel for reduction chunk k0 (nullptr: not a recording tap)
+    __device__ __forceinline__ uint32_t* in_bits_word(int m, int k0) const {
+        const int t = k0 / G::Ci, kh = t / 3, kw = t % 3;
+        if (kh == 0 || kw == 0 || m >= M) return nullptr;
+        const int n = m / kRowsPerSample, pix = m % kRowsPerSample;
+        const int ih = G::S * (pix / G::OH) + kh - 1, iw = G::S * (pix % G::OH) + kw - 1;
+        return in_bits + ((((long long)n * G::H + ih) * G::H + iw) * G::Ci + k0 % G::Ci) / 32;
+    }
     __device__ __forceinline__ float* c_row(int m) const { return out + (long long)m * G::Co; }
     __device__ __forceinline__ float* c_at(int m, int col) const { return out + (long long)m * G::Co + col; }
     __device__ __forceinline__ const float* mask_row(int) const { return nullptr; }
@@ -572,12 +589,13 @@ struct Dgrad {
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
     static constexpr bool A_TMA = true;  // A tile = one shifted TMA box of dy per chunk
+    static constexpr bool kInMaskBits = false, kMaskFromBits = true;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
     const CUtensorMap* tmap;
     const float* dy;
     const float* w;
-    const float* act;
+    const uint32_t* mbits;  // ReLU mask of the layer input as a bitmap (written by this layer's forward)
     float* dx;
     const float* img;
     int M, N, K, kbeg, m0, split;
@@ -592,7 +610,7 @@ struct Dgrad {
         dy = layer_dout<L>(p, v);
         tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 2 ? kTmDgr2 : kTmDgr3);
         w = v.w + G::OffW;
-        act = layer_out<L - 1>(p, v);
+        mbits = reinterpret_cast<const uint32_t*>(v.act + (L == 2 ? p.al.mk1 : p.al.mk2));
         dx = layer_dout<L - 1>(p, v);
         N = WImg<L>::DgrNTile;
         col0 = half * N;
@@ -640,12 +658,11 @@ struct Dgrad {
         return (((long long)n * G::H + ih) * G::H + iw) * G::Ci + cc % G::Ci;
     }
     __device__ __forceinline__ float* c_at(int r, int col) const { return dx + pix_off(r, col); }
-    __device__ __forceinline__ const float* mask_at(int r, int col) const { return act + pix_off(r, col); }
-    // masked epilogue: mask and output share the offset (input pixel, channel)
+    __device__ __forceinline__ const void* mask_at(int r, int col) const { return mbits + (pix_off(r, col) >> 5); }
+    // masked epilogue: the output element's offset (input pixel, channel) is also its mask bit;
+    // the 4 channels of a float4 lie in one 32-bit word
     __device__ __forceinline__ long long mask_off(int r, int col) const { return pix_off(r, col); }
-    __device__ __forceinline__ float4 mask4(long long off) const {
-        return __ldcs(reinterpret_cast<const float4*>(act + off));  // last use of the activation here
-    }
+    __device__ __forceinline__ uint32_t mask_word(int r, int col) const { return __ldg(mbits + (pix_off(r, col) >> 5)); }
     __device__ __forceinline__ void store_masked(int, int, long long off, float4 x) const {
         __stcs(reinterpret_cast<float4*>(dx + off), x);  // streaming: read next by another kernel
     }
@@ -658,6 +675,7 @@ struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = (L >= 2);
+    static constexpr bool kInMaskBits = false, kMaskFromBits = false;
     // TMA: a tile's 128 rows are 128 / Ci taps x Ci channels; one box per tap = 32 output pixels
     // (the chunk's reduction indices) x Ci channels, stored [tap][pixel][ci]
     static constexpr int kBoxes = 128 / G::Ci, kTmaCi = G::Ci;

@@ -50,7 +50,9 @@ struct WsPlan {
     static constexpr int BStage = N * 256;                          // hi + lo tiles
     static constexpr int Sacc = kBM * N * 4;                        // tile sums [row][N], 16-B units
                                                                     // XOR-swizzled by row
-    static constexpr int Fixed = Stages * BStage + 256 + Sacc;
+    // masked epilogues reading the ReLU mask as a bitmap stage the tile's words in shared memory
+    static constexpr int MaskWords = (Op::EPI == 1 && Op::kMaskFromBits) ? kBM * N / 32 : 0;
+    static constexpr int Fixed = Stages * BStage + 256 + Sacc + MaskWords * 4;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
     // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
     static constexpr int ARaw = (ARawMax > 8 ? 8 : ARawMax) & ~1;
@@ -58,7 +60,8 @@ struct WsPlan {
     static constexpr int ARawOff = Stages * BStage;
     static constexpr int BarOff = ARawOff + ARaw * kARawTile;
     static constexpr int SaccOff = BarOff + 256;
-    static constexpr int Bytes = SaccOff + Sacc;
+    static constexpr int MbitsOff = SaccOff + Sacc;
+    static constexpr int Bytes = MbitsOff + MaskWords * 4;
     // epilogue: one warp per TMEM lane quadrant (4), or two each draining half the columns (8)
     static constexpr int EpiWarps = Op::kEpiWarps;
     static_assert(EpiWarps == 4 || EpiWarps == 8, "epilogue warps");
@@ -391,6 +394,14 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
 #pragma unroll
                 for (int j = 0; j < 32; ++j) a[j] = k0 + j < klim ? 1.0f : 0.0f;
             }
+            if constexpr (Op::kInMaskBits) {
+                if (uint32_t* wdst = op.in_bits_word(m, k0)) {
+                    uint32_t wbits = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) wbits |= (a[j] > 0.0f ? 1u : 0u) << j;
+                    *wdst = wbits;
+                }
+            }
             // ---- wait until the MMAs of this stage's previous use are done
             SMX_TL(g * 8 + 2, gt == 0);
             if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
@@ -562,7 +573,19 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
-            if constexpr (Op::EPI == ctc::kEpiMask) {
+            // bitmap masks: the tile's words are loaded now (in flight during the drains) and staged
+            // in shared memory before the scatter
+            constexpr int kMW = Plan::MaskWords > 0 ? Plan::MaskWords / Plan::EpiThreads : 1;
+            uint32_t mword[kMW];
+            if constexpr (Plan::MaskWords > 0) {
+                static_assert(Plan::MaskWords % Plan::EpiThreads == 0, "mask-word mapping");
+                constexpr int WPR = Plan::N / 32;  // words per row
+#pragma unroll
+                for (int j = 0; j < kMW; ++j) {
+                    const int w = et + j * Plan::EpiThreads, m = mt0 + w / WPR;
+                    mword[j] = m < M ? op.mask_word(m, 32 * (w % WPR)) : 0u;
+                }
+            } else if constexpr (Op::EPI == ctc::kEpiMask) {
                 // warm L2 with the tile's ReLU-mask lines (one 128-byte line per 32 columns of a row)
                 const int m = mt0 + row;
                 if (m < M)
@@ -696,8 +719,28 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 // whole 128-byte pixel segments.  Mask loads are issued 8 rows ahead of their use.
                 constexpr int Q4 = Plan::N / 4, RSTEP = Plan::EpiThreads / Q4, PER = kBM / RSTEP, U = 8;
                 static_assert(Plan::EpiThreads % Q4 == 0 && PER % U == 0, "epilogue mapping");
+                uint32_t* sbits = reinterpret_cast<uint32_t*>(smem + Plan::MbitsOff);
+                if constexpr (Plan::MaskWords > 0) {
+#pragma unroll
+                    for (int j = 0; j < kMW; ++j) sbits[et + j * Plan::EpiThreads] = mword[j];
+                }
                 asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // the whole tile is in sacc
                 const int c4 = et % Q4, r0 = et / Q4;
+                if constexpr (Plan::MaskWords > 0) {
+                    // bits of the thread's 4 channels: word (row, column / 32), bit column % 32
+                    constexpr int WPR = Plan::N / 32;
+                    const int wc = (4 * c4) >> 5, sh = (4 * c4) & 31;
+#pragma unroll 4
+                    for (int ii = 0; ii < PER; ++ii) {
+                        const int r = r0 + RSTEP * ii, m = mt0 + r;
+                        if (m >= M || 4 * c4 >= N) continue;
+                        const uint32_t b = sbits[r * WPR + wc] >> sh;
+                        const float4 x = *s4(r, c4);
+                        op.store_masked(m, 4 * c4, op.mask_off(m, 4 * c4),
+                                        make_float4((b & 1u) ? x.x : 0.0f, (b & 2u) ? x.y : 0.0f, (b & 4u) ? x.z : 0.0f,
+                                                    (b & 8u) ? x.w : 0.0f));
+                    }
+                } else
                 for (int i0 = 0; i0 < PER; i0 += U) {
                     float4 mk[U];
                     long long off[U];

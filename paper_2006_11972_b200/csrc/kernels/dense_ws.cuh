@@ -25,6 +25,7 @@ struct DenseOp {
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
     static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false;
     static constexpr int kBoxes = 1, kTmaCi = 1;
+    static constexpr bool kInMaskBits = false, kMaskFromBits = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;
     const float* A;
     const float* B;
@@ -103,7 +104,7 @@ struct DenseOp {
             for (int j = 0; j < 4 && col + j < N; ++j) c[j] = v[j];
         }
     }
-    __device__ __forceinline__ const float* mask_at(int m, int col) const { return mask + (long long)m * ldmask + n0 + col; }
+    __device__ __forceinline__ const void* mask_at(int m, int col) const { return mask + (long long)m * ldmask + n0 + col; }
     __device__ __forceinline__ long long mask_off(int m, int col) const {
         return (long long)m * ldmask + n0 + col;
     }

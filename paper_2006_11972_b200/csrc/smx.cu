@@ -1174,7 +1174,7 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             cudaEventRecord(c->ev[6], c->stream);
             for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(c->jobs, n4);
             cudaEventRecord(c->ev[7], c->stream);
-        } else if ((kind == 2 || kind == 3) && c->cnn) {
+        } else if (kind >= 2 && kind <= 7 && c->cnn) {
             if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
             std::vector<int> v(n);
             for (int i = 0; i < n; ++i) v[i] = i;
@@ -1185,6 +1185,14 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             auto launch = [&] {
                 if (kind == 2) {
                     conv_forward<2>(c, a, n, c->d.max_batch);
+                } else if (kind == 4) {
+                    conv_dgrad<2>(c, a, n, c->d.max_batch);
+                } else if (kind == 5) {
+                    conv_dgrad<3>(c, a, n, c->d.max_batch);
+                } else if (kind == 6) {
+                    conv_forward<3>(c, a, n, c->d.max_batch);
+                } else if (kind == 7) {
+                    conv_wgrad<3>(c, a, n, c->d.max_batch);
                 } else if (c->d.gemm_mode == SMX_GEMM_TC) {  // the implicit GEMM alone (no split reduction)
                     using G = cnn::Geo<2>;
                     const int splits = (c->d.max_batch * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
