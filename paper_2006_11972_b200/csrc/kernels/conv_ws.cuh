@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 #ifdef SMX_DBG_TIMELINE
-    __shared__ int tl_flag;
+    int& tl_flag = reinterpret_cast<int*>(tmem_slot)[1];  // spare word of the barrier area
     if (threadIdx.x == 0)
         tl_flag = (blockIdx.x == 0 && blockIdx.y == 1 && blockIdx.z == 1) ? atomicExch(&smx_tl_armed, 0) : 0;
     __syncthreads();
@@ -650,16 +650,20 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         asm volatile("tcgen05.fence::before_thread_sync;");
                         mbar_arrive(&acce[acc_i]);
                     }
-                    for (int c0 = cbeg; c0 < cbeg + cw; c0 += 16) {
-                        uint32_t r[16];
+                    // 32 columns per TMEM round trip (two loads in flight before one wait)
+                    for (int c0 = cbeg; c0 < cbeg + cw; c0 += 32) {
+                        uint32_t r[32];
+                        const bool two = c0 + 16 < cbeg + cw;
                         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
+                        if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0 + 16, r + 16);
                         asm volatile("tcgen05.wait::ld.sync.aligned;");
-                        if (c0 + 16 >= cbeg + cw) {
+                        if (c0 + 32 >= cbeg + cw) {
                             asm volatile("tcgen05.fence::before_thread_sync;");
                             mbar_arrive(&acce[acc_i]);
                         }
 #pragma unroll
-                        for (int jj = 0; jj < 16; jj += 4) {
+                        for (int jj = 0; jj < 32; jj += 4) {
+                            if (jj >= 16 && !two) break;
                             float4* sp = s4(row, (c0 + jj) >> 2);
                             const float4 nv = make_float4(__uint_as_float(r[jj]), __uint_as_float(r[jj + 1]),
                                                           __uint_as_float(r[jj + 2]), __uint_as_float(r[jj + 3]));
