@@ -384,8 +384,10 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 }
             }
             __syncwarp();  // this warp's reads of the slot precede the refill below
-            if constexpr (Op::A_TMA)
-                if (lane == 0) mbar_arrive(&rawe[rd_slot]);
+            // (TMA operands: the slot is released only once the loaded registers have been
+            // consumed by the TMEM stores below; an arrive right after the LDS instructions could
+            // overtake loads still in flight, and the TMA warp would refill the slot under them)
+            const int a_slot = rd_slot;
             SMX_TL(g * 8 + 5, gt == 0);
             a_issue();
             rd_slot += 2;
@@ -446,6 +448,10 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             SMX_TL(g * 8 + 6, gt == 0);
             asm volatile("tcgen05.wait::st.sync.aligned;");
             SMX_TL(g * 8 + 4, gt == 0);
+            if constexpr (Op::A_TMA) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&rawe[a_slot]);
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;");
             asm volatile("fence.proxy.async.shared::cta;");
             asm volatile("tcgen05.fence::before_thread_sync;");

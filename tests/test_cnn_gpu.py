@@ -172,3 +172,24 @@ def test_engine_cnn_study_exact_vs_oracle(ds):
         o = ol.CnnSlot(ds, max_steps=8)
         o.train(hp_table(info["trials"][trial]), 6)
         assert [(s, l, a) for s, l, a in hist] == [(6, *o.eval())]
+
+
+def test_tc_determinism_many_slots(ds):
+    """Run-to-run bitwise determinism at a full active set (64 slots, mixed batch sizes): many
+    CTAs per kernel and a deep TMA ring, where a released-too-early operand slot shows up as
+    differing gradients (profiles/debug/race_probe.py is the longer version)."""
+    del ds
+    ref = None
+    for _ in range(3):
+        with ex.Executor(n_slots=64, n_ckpts=2, gemm_mode=ex.GEMM_TC, max_steps=8, max_batch=128, n_train=8192,
+                         n_val=256, model=ex.MODEL_CNN) as e:
+            for s in range(64):
+                e.slot_init(s)
+                e.hp_upload(s, 0, np.tile(np.float32([0.05, 0.9, 1e-4, 128 if s % 2 == 0 else 64]), (8, 1)))
+            e.train(list(range(64)), 1)
+            ms = [e.slot_read(s)[1].copy() for s in range(64)]
+        if ref is None:
+            ref = ms
+        else:
+            bad = [s for s in range(64) if not np.array_equal(ms[s], ref[s])]
+            assert not bad, f"slots with run-to-run differences: {bad}"
