@@ -1,10 +1,11 @@
 """Back-to-back tcgen05.mma kind::tf32 rate (see mma_rate.cu)."""
 import ctypes
+import sys
 from pathlib import Path
 
 lib = ctypes.CDLL(str(Path(__file__).with_name("mma_rate.so")))
 iters = 2000
-for ts in (1,):
+for ts in ((1, 0) if "ss" in sys.argv[1:] else (1,)):
     for n in (64, 128):
         cyc = (ctypes.c_longlong * 148)()
         ms = ctypes.c_float()
