@@ -10,11 +10,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
-__device__ __forceinline__ uint32_t idesc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ uint32_t idesc(int n, int m = 128) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-template <bool TS, int N>
+template <bool TS, int N, int M = 128>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, long long* cycles) {
     extern __shared__ __align__(1024) char smem[];
     __shared__ uint32_t tslot;
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, long long* cycles)
     if (threadIdx.x == 0) {
         const uint32_t lbo = N * 16, sb = su32(smem), sa = sb + 32768;
         const uint64_t db = sdesc(sb, lbo, 128), da = sdesc(sa, 128 * 16, 128);
-        const uint32_t id = idesc(N);
+        const uint32_t id = idesc(N, M);
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -80,6 +80,11 @@ extern "C" int run(int ts, int n, int iters, long long* host_cycles, float* ms) 
     if (!ts && n == 64) go(mma_rate<false, 64>);
     if (!ts && n == 128) go(mma_rate<false, 128>);
     if (!ts && n == 256) go(mma_rate<false, 256>);
+    // M = 64 (ts 2: TS, ts 3: SS)
+    if (ts == 2 && n == 128) go(mma_rate<true, 128, 64>);
+    if (ts == 2 && n == 256) go(mma_rate<true, 256, 64>);
+    if (ts == 3 && n == 128) go(mma_rate<false, 128, 64>);
+    if (ts == 3 && n == 256) go(mma_rate<false, 256, 64>);
     cudaEventSynchronize(b);
     cudaEventElapsedTime(ms, a, b);
     cudaMemcpy(host_cycles, d, 148 * sizeof(long long), cudaMemcpyDeviceToHost);
