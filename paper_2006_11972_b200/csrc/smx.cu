@@ -255,7 +255,7 @@ constexpr int conv_tpc<cnn::ctc::Fwd<1>>() { return 8; }
 template <>
 constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 16; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 8; }
+constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 4; }
 template <>
 constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 16; }
 template <>
