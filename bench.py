@@ -383,7 +383,9 @@ def main():
         kx.hp_upload(s_, 0, np.tile(np.float32([0.05, 0.9, 1e-4, 128]), (64, 1)))
     kx.train(list(range(n_k)), 1)  # produce activations / gradients once
     kx.sync()
-    ms = {kind: kx.bench_kernel(kind, n_k, 30) for kind in (2, 3)}
+    # CNN: 2 / 3 = conv2 forward / weight gradient, 4 / 5 = conv2 / conv3 input gradient, 6 = conv3
+    # forward, 7 = conv3 weight gradient (+ its split reduction); MLP: 2 / 3 only
+    ms = {kind: kx.bench_kernel(kind, n_k, 30) for kind in ((2, 3, 4, 5, 6, 7) if cnn else (2, 3))}
     # HBM-bound kernels on a working set > 3x the 126 MB L2 (many small slots / checkpoints)
     n_h = int(np.ceil(3 * 126e6 / (20 * kx.p_algo * 1.0) / 16)) * 16
     kh = ex.Executor(n_slots=n_h, n_ckpts=n_h, device=local, max_steps=8, gemm_mode=gemm_mode, max_batch=8,
@@ -421,6 +423,12 @@ def main():
         kernels = {
             "K1_conv2_fwd": tensor("fwd", gemm_flops, ms[2]),
             "K3_conv2_wgrad": tensor("wgrad", gemm_flops, ms[3]),
+            # every conv2 / conv3 implicit GEMM has the same algorithmic product count per sample
+            # (2 x 256 x 64 x 288 = 2 x 64 x 128 x 576); the input gradients issue 16/9 of it
+            "K2_conv2_dgrad": tensor("dgrad2", gemm_flops, ms[4]),
+            "K2_conv3_dgrad": tensor("dgrad3", gemm_flops, ms[5]),
+            "K1_conv3_fwd": tensor("fwd3", gemm_flops, ms[6]),
+            "K3_conv3_wgrad": tensor("wgrad3", gemm_flops, ms[7]),
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
