@@ -432,7 +432,7 @@ def main():
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
-        # the largest single kernel of a lockstep (profiles/r01/launches_bench_c2.txt): the conv2
+        # the largest kernel share of the bench (profiles/r01/launches_bench_c2_mid.txt): the conv2
         # weight gradient, M 288 (tap, cin) x N 64 (cout) x K 32768 (sample, pixel) per group
         roofline = dict(kernels["K3_conv2_wgrad"])
         roofline["kernel"] = ("conv_ws_kernel<Wgrad<2>> (conv2 weight-gradient implicit GEMM, 64 groups x M 288 x "
