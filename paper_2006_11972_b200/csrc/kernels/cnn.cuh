@@ -616,7 +616,9 @@ struct Dgrad {
         col0 = half * N;
         img = v.act + (L == 2 ? p.al.wd2 : p.al.wd3) + (long long)half * WImg<L>::DgrChunks * N * 64;
         M = v.bs * HH * HH;
-        K = 4 * G::Co;
+        // an N tile of one parity row pi (conv3: 2 classes x 64 cin) has no taps from the
+        // neighbours below (da = 1) when pi = 0: its reduction stops after (da = 0, db = 0 / 1)
+        K = (N == 2 * G::Ci && half == 0) ? 2 * G::Co : 4 * G::Co;
         kbeg = 0;
         split = 0;
     }
