@@ -6,6 +6,8 @@ Outputs (git-ignored, but shipped to the GPU box by gpurun's snapshot):
     paper_2006_11972_b200/libsmx.so               executor: CUDA kernels + C ABI (include/smx.h)
     paper_2006_11972_b200/_stagemerge*.so         host library (C++ stagemerge API) + Python binding
     oracle/liboracle.so                           CPU oracle (test infrastructure)
+    tests/native/_stagemerge_stub*.so             host library over a host-only smx stub (CPU tests of the
+                                                  engine / scheduler; test infrastructure, not shipped)
     oracle/_ref/libstagemerge_ref.so              reference hpseq/plan, only when /root/reference exists
 """
 from __future__ import annotations
@@ -83,6 +85,39 @@ def build_host(force: bool = False) -> Path | None:
     return out
 
 
+def _host_flags():
+    import pybind11
+
+    return ["-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wextra", "-fvisibility=hidden",
+            f"-I{INCLUDE}", f"-I{CSRC / 'host'}", f"-I{NLOHMANN}", f"-I{pybind11.get_include()}",
+            f"-I{sysconfig.get_paths()['include']}"]
+
+
+STUB_DIR = ROOT / "tests" / "native"
+
+
+def build_stub(force: bool = False) -> Path | None:
+    """Test-only build: the host library objects + tests/native/smx_stub.cpp (a CPU stand-in for
+    every smx_* entry point) as the Python module `_stagemerge_stub`, so the engine's scheduling
+    properties are testable without a GPU.  Never imported by the product package."""
+    stub = STUB_DIR / "smx_stub.cpp"
+    if not stub.exists():
+        return None
+    out = STUB_DIR / ("_stagemerge_stub" + sysconfig.get_config_var("EXT_SUFFIX"))
+    objdir = PKG / "build" / "host"
+    objs = [objdir / (s.stem + ".o") for s in HOST_SOURCES if s.stem != "bind"]
+    deps = HOST_DEPS + [stub, INCLUDE / "smx.h", *objs]
+    if not (force or _stale(out, deps)):
+        return out
+    flags = _host_flags()
+    bind_obj = objdir / "bind_stub.o"
+    stub_obj = objdir / "smx_stub.o"
+    _run(["g++", *flags, "-DSMH_MODULE=_stagemerge_stub", "-c", "-o", bind_obj, CSRC / "host" / "bind.cpp"])
+    _run(["g++", *[f for f in flags if f != "-fvisibility=hidden"], "-c", "-o", stub_obj, stub])
+    _run(["g++", "-shared", "-o", out, *objs, bind_obj, stub_obj])
+    return out
+
+
 def build_oracle(force: bool = False) -> None:
     args = ["make", "-C", ROOT / "oracle"]
     if force:
@@ -95,6 +130,7 @@ def build_oracle(force: bool = False) -> None:
 def build_all(force: bool = False) -> None:
     build_smx(force)
     build_host(force)
+    build_stub(force)
     build_oracle(force)
 
 

@@ -12,7 +12,13 @@ std::string call(const std::string& text);
 
 void bind_engine(pybind11::module_& m);
 
-PYBIND11_MODULE(_stagemerge, m) {
+// The test build (tests/native, linked against the host-only smx stub instead of libsmx.so)
+// compiles this file again with -DSMH_MODULE=_stagemerge_stub.
+#ifndef SMH_MODULE
+#define SMH_MODULE _stagemerge
+#endif
+
+PYBIND11_MODULE(SMH_MODULE, m) {
     m.doc() = "stagemerge host library (C++20) over the smx B200 executor";
     m.def("call", &stagemerge::api::call, "JSON command interface (same commands as the reference shim)");
     bind_engine(m);

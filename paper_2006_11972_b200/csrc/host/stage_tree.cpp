@@ -20,7 +20,16 @@ ResumePoint find_latest_checkpoint(const SearchPlan& plan, NodeId node, StepCoun
     ResumePoint rp;
     const PlanNode& n = plan.node(node);
     if (running && running->count(node)) {
-        rp.kind = ResumeKind::kBlocked;  // Alg. 1 lines 15-16
+        // Alg. 1 lines 15-16: a running config blocks the request -- unless the in-flight worker
+        // has already saved the exact step asked for, in which case that NewCheckpoint unlocks it
+        // (acceptance 8).  Any other step stays blocked: the
+        // running worker will produce it.
+        if (n.ckpts.count(step) && step > n.start_step) {
+            rp.kind = ResumeKind::kCheckpoint;
+            rp.ckpt = CkptRef{node, step};
+        } else {
+            rp.kind = ResumeKind::kBlocked;
+        }
     } else if (auto it = n.ckpts.upper_bound(step); it != n.ckpts.begin() && std::prev(it)->first > n.start_step) {
         rp.kind = ResumeKind::kCheckpoint;  // scan step, step-1, ..., start (lines 21-24)
         rp.ckpt = CkptRef{node, std::prev(it)->first};

@@ -57,3 +57,15 @@ def test_open_without_gpu_fails_loudly():
 def test_struct_sizes():
     assert ctypes.sizeof(ex.ModelDesc) == 32
     assert ctypes.sizeof(ex.Stats) == 8 * 11
+
+
+def test_host_stub_covers_the_whole_abi():
+    """The CPU test stand-in (tests/native/smx_stub.cpp) implements every declared entry point,
+    so the engine tests run against the same ABI the product links."""
+    import glob
+
+    libs = glob.glob(str(ROOT / "tests" / "native" / "_stagemerge_stub*.so"))
+    assert libs, "run python -m paper_2006_11972_b200.build"
+    lib = ctypes.CDLL(libs[0])
+    for name in declared():
+        assert hasattr(lib, name), name
