@@ -63,7 +63,7 @@ auto translate(F&& f) -> decltype(f()) {
 }  // namespace
 
 void bind_engine(py::module_& m) {
-    py::class_<Engine>(m, "Engine")
+    py::class_<Engine>(m, "Engine", py::module_local())
         .def(py::init([](const std::string& key_json, const std::string& opts_json) {
                  const json k = json::parse(key_json);
                  CompatKey key{k.at("model").get<std::string>(), k.at("dataset").get<std::string>(),
@@ -155,7 +155,7 @@ void bind_engine(py::module_& m) {
     struct PyTuner {
         std::unique_ptr<Tuner> t;
     };
-    py::class_<PyTuner>(m, "Tuner")
+    py::class_<PyTuner>(m, "Tuner", py::module_local())
         .def(py::init([](const std::string& spec_json) {
             return translate([&] {
                 const StudySpec spec = parse_study(spec_json);

@@ -59,6 +59,15 @@ __global__ void gen_labels_kernel(const float* x, int* y, long long rows, uint64
     }
 }
 
+// Is every value tf32-exact (low 13 mantissa bits zero)?  An uploaded dataset that is not must
+// not take the tensor-core GEMMs' single-MMA data path (dense_ws.cuh A_EXACT / B_EXACT).
+__global__ void tf32_inexact_kernel(const uint32_t* v, long long n, int* flag) {
+    uint32_t acc = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc |= __ldcs(v + i) & 0x1FFFu;
+    if (__any_sync(0xffffffffu, acc != 0) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // ---- K10: seeded He-uniform init (identical for every root: prefix_digest(cfg,0) is
 // config independent, reference hpseq.cpp:591-607) ---------------------------------------
 __global__ void init_kernel(float* w, float* m, uint64_t seed, float s1, float s2, float s3) {

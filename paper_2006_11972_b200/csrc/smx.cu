@@ -76,6 +76,11 @@ struct smx_ctx {
     CopyJob* jobs = nullptr;    // device job list for fork copies
     int jobs_cap = 0;
     std::vector<char> ck_valid;
+    // every training / validation input value is exact in tf32 (true for the synthetic k/128
+    // data; re-checked on every smx_dataset_upload): only then may the tensor-core GEMMs skip
+    // the data operand's lo MMA
+    bool data_tf32_exact = true;
+    int* flag = nullptr;  // device scratch int
 
     struct Graph {
         int* d_slots = nullptr;
@@ -123,17 +128,23 @@ GemmArgs base_args(smx_ctx* c, const int* d_slots) {
 }
 
 // Tensor-core GEMMs of the MLP: the warp-specialised tcgen05 kernel (conv_ws.cuh) with the dense
-// Op policy (dense_ws.cuh); operands flagged as synthetic data are exact in tf32 and skip their
-// lo MMA.
+// Op policy (dense_ws.cuh); a data operand skips its lo MMA only while the context's dataset is
+// verified tf32-exact (smx_ctx::data_tf32_exact).
+// cudaFuncSetAttribute is per device: one bit per device that has the kernel configured
+template <class Op>
+void configure_ws(smx_ctx* c) {
+    static unsigned long long configured = 0;  // calls on one context come from one thread (smx.h)
+    const unsigned long long bit = 1ull << (c->device & 63);
+    if (configured & bit) return;
+    ck(cudaFuncSetAttribute(cnn::ws::conv_ws_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            cnn::ws::ws_smem<Op>()),
+       "conv_ws smem attribute");
+    configured |= bit;
+}
+
 template <class Op>
 void dense_ws_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
-    static bool configured = false;
-    if (!configured) {
-        ck(cudaFuncSetAttribute(cnn::ws::conv_ws_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cnn::ws::ws_smem<Op>()),
-           "dense smem attribute");
-        configured = true;
-    }
+    configure_ws<Op>(c);
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
     dim3 grid((a.N + 127) / 128, mtiles, groups);
     cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::WsPlan<Op>::Threads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, 1);
@@ -147,10 +158,10 @@ void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
     constexpr int wepi = EPI == tc::kTcStore ? dws::kEpiStore : EPI == tc::kTcBiasRelu ? dws::kEpiBiasRelu
                          : EPI == tc::kTcBias ? dws::kEpiBias : EPI == tc::kTcMask ? dws::kEpiMask : dws::kEpiPartT;
     if constexpr (AM == 0 && BMODE == 0 && EPI == tc::kTcBiasRelu) {
-        if (a.a.from_data) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, true, false>>(c, a, groups, m_max);
+        if (a.a.from_data && c->data_tf32_exact) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, true, false>>(c, a, groups, m_max);
     }
     if constexpr (AM == 1 && BMODE == 1 && EPI == tc::kTcStore) {
-        if (a.b.from_data) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, true>>(c, a, groups, m_max);
+        if (a.b.from_data && c->data_tf32_exact) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, true>>(c, a, groups, m_max);
     }
     dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, false>>(c, a, groups, m_max);
 }
@@ -263,13 +274,7 @@ constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 8; }
 
 template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
-    static bool configured = false;
-    if (!configured) {
-        ck(cudaFuncSetAttribute(cnn::ws::conv_ws_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                cnn::ws::ws_smem<Op>()),
-           "conv smem attribute");
-        configured = true;
-    }
+    configure_ws<Op>(c);
     // tiles per CTA: as many as the Op likes (fewer pipeline fills) while the grid still gives
     // every SM at least two CTAs; it changes only the work split, never the arithmetic
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
@@ -725,6 +730,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             ck(cudaMalloc(&c->eval_out, sizeof(double) * 2 * kEvalChunk), "eval out");
             ck(cudaMalloc(&c->eval_slots, sizeof(int) * kEvalChunk), "eval slots");
             ck(cudaMalloc(&c->scratch_slots, sizeof(int) * n_slots), "scratch slots");
+            ck(cudaMalloc(&c->flag, sizeof(int)), "flag");
             ck(cudaMemsetAsync(c->grad, 0, sizeof(float) * c->palloc * n_slots, c->stream), "grad zero");
             ck(cudaMemsetAsync(c->hp, 0, sizeof(float) * 4 * (long long)d.max_steps * n_slots, c->stream), "hp zero");
             ck(cudaMemsetAsync(c->loss, 0, sizeof(float) * (long long)d.max_steps * n_slots, c->stream), "loss zero");
@@ -750,7 +756,7 @@ int smx_close(smx_ctx* c) {
     free_graphs(c);
     void* bufs[] = {c->slab, c->grad, c->pool, c->st, c->ck_st, c->hp, c->loss, c->act, c->xtrain, c->ytrain,
                     c->xval, c->yval, c->eval_act, c->zval, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
-                    c->scratch_slots, c->tmaps};
+                    c->scratch_slots, c->tmaps, c->flag};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& e : c->ev)
@@ -810,7 +816,20 @@ int smx_dataset_upload(smx_ctx* c, const float* x, const int32_t* y, const float
         ck(cudaMemcpyAsync(c->xval, vx, sizeof(float) * (long long)c->d.n_val * c->d_in, cudaMemcpyHostToDevice, c->stream),
            "vx H2D");
         ck(cudaMemcpyAsync(c->yval, vy, sizeof(int) * c->d.n_val, cudaMemcpyHostToDevice, c->stream), "vy H2D");
+        // tf32-exactness of the new inputs decides the GEMM path; captured graphs embed it
+        ck(cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream), "flag zero");
+        tf32_inexact_kernel<<<592, 256, 0, c->stream>>>(reinterpret_cast<const uint32_t*>(c->xtrain), rows * c->d_in,
+                                                        c->flag);
+        launch_check(c, "tf32 check train");
+        tf32_inexact_kernel<<<148, 256, 0, c->stream>>>(reinterpret_cast<const uint32_t*>(c->xval),
+                                                        (long long)c->d.n_val * c->d_in, c->flag);
+        launch_check(c, "tf32 check val");
+        int inexact = 0;
+        ck(cudaMemcpyAsync(&inexact, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flag D2H");
         ck(cudaStreamSynchronize(c->stream), "dataset sync");
+        const bool exact = inexact == 0;
+        if (exact != c->data_tf32_exact) free_graphs(c);
+        c->data_tf32_exact = exact;
     });
 }
 
