@@ -38,7 +38,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 TRAFFIC: dict = {
     # profiles/r01/ncu_conv2_fwd_full.txt: 64 groups at bs 128 (= the bench's roofline launch)
     "conv_ws_kernel<Fwd<2>>": 1_083_516_000 + 506_999_552,
-    # profiles/r01/ncu_ws_full.txt: conv2 weight-gradient GEMM, 64 groups at bs 128
+    # profiles/r01/ncu_wgrad2_full.txt: conv2 weight-gradient GEMM, 64 groups at bs 128
     "conv_ws_kernel<Wgrad<2>>": 1_674_893_000 + 75_405_000,
 }
 METRIC = "trial-equivalent train steps/sec per study"
@@ -189,73 +189,78 @@ def cuda_time(fn, world):
     return reduce_max(a.elapsed_time(b) / 1e3, world), out
 
 
-def cpu_baseline(specs, trial_per_stage: float, seconds: float = 12.0) -> dict:
-    """The CPU oracle trainer (oracle/liboracle.so, OpenMP over all host cores) on a bounded
-    sample of the workload: the first stage-steps of the study's first trials.  Reported in the
-    metric's unit by scaling unique stage-steps/s with the same merge ratio the plan gives the
-    GPU run (the CPU executor would execute the identical plan)."""
-    import ctypes
-
-    import oracle_lib as ol
-    from paper_2006_11972_b200 import host
-
-    info = host.expand_study(specs[0])
-    cnn = info["key"]["model"] == "cnn"
-    cores = os.cpu_count() or 1
-    n = max(cores, 8)
-    hp = []
-    for cfg in info["trials"][:n]:
-        r = host.call({"op": "sequence", "config": cfg})
-        rows = np.zeros((cfg["total_steps"], 4), np.float32)
-        for c, name in enumerate(("lr", "momentum", "weight_decay", "batch_size")):
-            rows[:, c] = r["hps"][name]["values"] if name in r["hps"] else [0.1, 0.9, 0.0, 128][c]
-        hp.append(rows)
-    ds = ol.cnn_dataset(65536, 4096, 128) if cnn else ol.dataset()
-    T = min(int(info["max_steps"]), 2000)
-    slots = [ol.CnnSlot(ds, max_steps=T + 1) for _ in range(n)] if cnn else [ol.Slot(max_steps=T + 1) for _ in range(n)]
-    lib = ol.oracle()
-    train_many = lib.orc_cnn_train_many if cnn else lib.orc_train_many
-    FP = ctypes.POINTER(ctypes.c_float)
-    W = (FP * n)(*[ol.fp(s.w) for s in slots])
-    M = (FP * n)(*[ol.fp(s.m) for s in slots])
-    H = (FP * n)(*[ol.fp(h) for h in hp])
-    L = (FP * n)(*[ol.fp(s.loss) for s in slots])
-    step = (ctypes.c_int64 * n)()
-    off = (ctypes.c_int64 * n)()
-    done, t0 = 0, time.perf_counter()
-    k = 1 if cnn else 2
-    while time.perf_counter() - t0 < seconds and done + k <= T:
-        rc = train_many(n, W, M, step, off, H, T, k, ol.fp(ds.x), ds.y.ctypes.data, ds.n_train, L, cores)
-        assert rc == 0
-        done += k
-    dt = time.perf_counter() - t0
-    stage_steps = n * done
-    return {"value": stage_steps / dt * trial_per_stage, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{stage_steps} stage-steps ({n} trials x {done} steps of {info['name']}, OpenMP over {cores} threads) in "
-                      f"{dt:.1f}s = {stage_steps / dt:.1f} stage-steps/s, x{trial_per_stage:.3f} trial-steps per "
-                      f"stage-step (the plan's merge ratio)"}
+def _spec_text(name: str) -> str:
+    return (ROOT / "paper_2006_11972_b200" / "studies" / f"{WORKLOADS[name][0]}.json").read_text()
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle port of the executor on the same plan)."""
-    if rank != 0:
+class CpuReference:
+    """The reference's CPU path for a workload (oracle/cpu_executor.py): the merged plan built by
+    the compiled reference (oracle/_ref: SearchPlan::insert_trial / value_at), executed with the
+    stage executor's resume / fork / eval semantics by the CPU oracle trainer (liboracle_v4.so,
+    AVX-512, when the host has it) on every host core.  Imports nothing from
+    paper_2006_11972_b200.  A sample runs the plan from scratch for a bounded wall budget; TES is
+    the study's trial-steps x (executed / unique stage-steps) / wall seconds."""
+
+    def __init__(self, workload_name: str, max_batch: int):
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import cpu_executor as cx
+
+        self.cx = cx
+        spec = json.loads(_spec_text(workload_name))
+        if spec.get("tuner"):
+            raise ValueError("the CPU reference executes untuned plans only")
+        self.info = cx.expand_study(spec)
+        self.plan = cx.reference_plan(self.info["key"], self.info["trials"])
+        self.lib = cx.oracle_lib()
+        self.model = cx.Model(self.info["key"]["model"], self.lib, n_train=65536, max_batch=max_batch, n_val=4096)
+        self.cores = os.cpu_count() or 1
+        self.unique = sum(n["hi"] - n["start"] for n in self.plan["node_values"])
+        self.trial_steps = cx.total_trial_steps(self.plan)
+
+    def sample(self, budget_s: float) -> dict:
+        r = self.cx.run_plan(self.plan, self.model, eval_interval=self.info["eval_interval"], threads=self.cores,
+                             budget_s=budget_s)
+        frac = r["executed"] / self.unique
+        tes = self.trial_steps * frac / r["wall_s"]
+        return {"value": tes, "unit": UNIT, "cores": self.cores, "kind": "port",
+                "same_config": True, "fraction_executed": frac,
+                "sample": f"{self.info['name']}: the reference-built plan ({len(self.plan['node_values'])} nodes, "
+                          f"{self.unique} unique stage-steps, {self.trial_steps} trial-steps) executed from scratch "
+                          f"for a {budget_s:.0f} s wall budget: {r['executed']} stage-steps + "
+                          f"{len(r['metrics'])} evals in {r['wall_s']:.1f} s ({frac * 100:.2f} % of the study; "
+                          f"{r['executed'] / r['wall_s']:.1f} stage-steps/s) on {self.cores} threads, "
+                          f"oracle {self.lib.isa}; TES = trial-steps x fraction / wall",
+                "executed_stage_steps": r["executed"], "wall_s": r["wall_s"]}
+
+    @staticmethod
+    def libraries() -> list:
+        maps = Path("/proc/self/maps")
+        if not maps.exists():
+            return []
+        return sorted({l.split()[-1] for l in maps.read_text().splitlines() if l.endswith(".so") and str(ROOT) in l})
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path (CpuReference), rank 0
+    only (other ranks exit 0 without work); nothing of paper_2006_11972_b200 is imported."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    specs, _, desc = workload(args.workload, 1)
-    from paper_2006_11972_b200 import host
-
-    info = host.expand_study(specs[0])
-    ratio = info["total_steps"] / info["unique_steps"]
-    vals = []
+    desc = WORKLOADS[args.workload][2].format(n=1, n1=0, ies="y")
+    ref = CpuReference(args.workload, WORKLOADS[args.workload][4])
+    budget = max(3.0, min(20.0, 150.0 / (args.warmup + args.steps)))
+    vals, cb = [], None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(specs, ratio, seconds=4.0)
+        cb = ref.sample(budget)
         if i >= args.warmup:
             vals.append(cb["value"])
     v = float(np.mean(vals))
+    libs = CpuReference.libraries()
+    assert not any("paper_2006_11972_b200" in l for l in libs), libs
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                       "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
                       "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                      "config": {"workload": desc, "flush": "n/a (CPU)"},
-                      "cpu_baseline": {**cb, "value": v},
+                      "config": {"workload": desc, "flush": "n/a (CPU)", "same_config": True},
+                      "cpu_baseline": {**cb, "value": v}, "native_so_loaded": libs,
                       "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
           flush=True)
 
@@ -274,9 +279,9 @@ def main():
     args = ap.parse_args()
     if not args.slots:
         args.slots = WORKLOADS[args.workload][3]
-    rank, world, local = dist_init()
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args)
+    rank, world, local = dist_init()
 
     import torch
 
@@ -318,23 +323,26 @@ def main():
     value = trial_steps * args.steps / t
 
     # ---- e2e: the same study through the public Engine API with the dataset coming from
-    # pinned host memory every step (H2D inside the timed region) and metrics read back (D2H)
+    # pinned host memory every step (H2D inside the timed region) and metrics read back (D2H).
+    # The host copy is staged once, outside the timed region, by reading the context's dataset
+    # back (smx_dataset_read) into page-locked buffers.
     import ctypes
 
-    import oracle_lib as ol
-
-    # host copy of the dataset (bit-identical to the on-device generator)
-    ds = ol.cnn_dataset(65536, 4096, max_batch) if cnn else ol.dataset()
     lib = ex.load_library()
-    pinned = []
-    host_arrays = []
-    for a in (ds.x, ds.y, ds.vx, ds.vy):
+    d_in = 32 * 32 * 4 if cnn else 784
+    rows = 65536 + max_batch
+    shapes = [((rows, d_in), np.float32), ((rows,), np.int32), ((4096, d_in), np.float32), ((4096,), np.int32)]
+    pinned, host_arrays = [], []
+    for shape, dt in shapes:
+        nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
         p = ctypes.c_void_p()
-        assert lib.smx_host_alloc(a.nbytes, ctypes.byref(p)) == 0
-        buf = np.ctypeslib.as_array((ctypes.c_byte * a.nbytes).from_address(p.value)).view(a.dtype).reshape(a.shape)
-        buf[...] = a
+        assert lib.smx_host_alloc(nbytes, ctypes.byref(p)) == 0
+        host_arrays.append(np.ctypeslib.as_array((ctypes.c_byte * nbytes).from_address(p.value)).view(dt).reshape(shape))
         pinned.append(p)
-        host_arrays.append(buf)
+    ctx0 = ctypes.c_void_p(eng.context_ptrs()[0])
+    ex._check(lib.smx_dataset_read(ctx0, *[a.ctypes.data_as(ctypes.POINTER(ctypes.c_float)) if a.dtype == np.float32
+                                           else a.ctypes.data for a in host_arrays]))
+    digest0 = eng.dataset_digest()
 
     def one_e2e():
         eng.reset()
@@ -345,9 +353,10 @@ def main():
     one_e2e()
     te, st_e = cuda_time(lambda: [one_e2e() for _ in range(args.steps)][-1], world)
     e2e_value = reduce_sum(st_e["trial_steps"], world) * args.steps / te
+    assert eng.dataset_digest() == digest0, "e2e upload changed the dataset"
+    del host_arrays
     for p in pinned:
         lib.smx_host_free(p)
-    eng.upload_dataset(*[np.ascontiguousarray(a) for a in (ds.x, ds.y, ds.vx, ds.vy)])
 
     # ---- GPU-second savings: the same studies unmerged (TRIAL mode: every trial on its own
     # path) on the same executor, device-timed once after one warm-up run
@@ -449,8 +458,8 @@ def main():
     roofline["traffic"] = TRAFFIC.get(roofline["kernel"].split(" ")[0])
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(specs, trial_steps / stage_steps)
+    if rank == 0 and not args.no_cpu and not tuned and world == 1:
+        cpu = CpuReference(args.workload, max_batch).sample(20.0)
 
     if rank == 0:
         line = {

@@ -111,6 +111,9 @@ int smx_dataset_digest(smx_ctx* ctx, uint64_t* out);
  * y int32 labels, vx n_val x d_in, vy.  Host->device
  * copies on the context stream; pinned buffers (smx_host_alloc) make them DMA-direct. */
 int smx_dataset_upload(smx_ctx* ctx, const float* x, const int32_t* y, const float* vx, const int32_t* vy);
+/* Device -> host copy of the context's dataset in the smx_dataset_upload layout (e.g. to stage
+ * the synthetic set in pinned memory for the end-to-end path); synchronous. */
+int smx_dataset_read(smx_ctx* ctx, float* x, int32_t* y, float* vx, int32_t* vy);
 /* Page-locked host buffers for the e2e path. */
 int smx_host_alloc(uint64_t bytes, void** out);
 int smx_host_free(void* p);

@@ -132,16 +132,20 @@ typedef struct {
 } Work;
 
 /* out[n][p][co] = relu(b[co] + sum_{t valid asc} sum_{ci < Cr asc} in[n][q(p,t)][ci] * W[co][t][ci]) */
+/* nt > 1: samples split over OpenMP threads -- every output is still its own sequential chain, so
+ * the result is bitwise the nt == 1 result (tested). */
 static void conv_fwd(int l, const float* restrict in, int B, const float* restrict w, float* restrict out,
-                     Work* wk) {
+                     Work* wk, int nt) {
     const int H = LH[l], Ci = LCI[l], Cr = LCR[l], Co = LCO[l], S = LS[l], OH = H / S;
     for (int co = 0; co < Co; ++co)
         for (int t = 0; t < 9; ++t)
             for (int ci = 0; ci < Ci; ++ci) wk->wt[((long)t * Ci + ci) * Co + co] = w[OW[l] + ((long)co * 9 + t) * Ci + ci];
-    float acc[128];
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int n = 0; n < B; ++n)
         for (int oh = 0; oh < OH; ++oh)
             for (int ow = 0; ow < OH; ++ow) {
+                float acc[128];
                 for (int co = 0; co < Co; ++co) acc[co] = 0.0f;
                 for (int t = 0; t < 9; ++t) {
                     const int ih = oh * S + t / 3 - 1, iw = ow * S + t % 3 - 1;
@@ -161,42 +165,55 @@ static void conv_fwd(int l, const float* restrict in, int B, const float* restri
             }
 }
 
-/* gW[co][t][ci] = sum_{n asc, p asc, valid} dy[n][p][co] * in[n][q(p,t)][ci];  gb[co] = sum dy */
+/* gW[co][t][ci] = sum_{n asc, p asc, valid} dy[n][p][co] * in[n][q(p,t)][ci];  gb[co] = sum dy
+ * Accumulated as acc[t][ci][co] (the co loop innermost: contiguous in dy and acc, so it
+ * vectorises); the (t, ci) rows are split over OpenMP threads when nt > 1.  Every (co, t, ci)
+ * chain keeps its (n asc, p asc) order, so the result is bitwise the nt == 1 result (tested). */
 static void conv_wgrad(int l, const float* restrict in, const float* restrict dy, int B, float* restrict grad,
-                       Work* wk) {
+                       Work* wk, int nt) {
     const int H = LH[l], Ci = LCI[l], Cr = LCR[l], Co = LCO[l], S = LS[l], OH = H / S;
-    float* restrict acc = wk->acc; /* [co][t][ci] */
+    float* restrict acc = wk->acc; /* [t][ci][co] */
     memset(acc, 0, sizeof(float) * (size_t)Co * 9 * Ci);
     float gb[128];
     for (int co = 0; co < Co; ++co) gb[co] = 0.0f;
-    for (int n = 0; n < B; ++n)
-        for (int oh = 0; oh < OH; ++oh)
-            for (int ow = 0; ow < OH; ++ow) {
-                const float* d = dy + (((long)n * OH + oh) * OH + ow) * Co;
-                for (int co = 0; co < Co; ++co) gb[co] = gb[co] + d[co];
-                for (int t = 0; t < 9; ++t) {
-                    const int ih = oh * S + t / 3 - 1, iw = ow * S + t % 3 - 1;
-                    if (ih < 0 || ih >= H || iw < 0 || iw >= H) continue;
-                    const float* restrict xin = in + (((long)n * H + ih) * H + iw) * Ci;
-                    for (int co = 0; co < Co; ++co) {
-                        const float dv = d[co];
-                        float* restrict a = acc + ((long)co * 9 + t) * Ci;
-                        for (int ci = 0; ci < Cr; ++ci) a[ci] = fmaf(dv, xin[ci], a[ci]);
+    const int rows = 9 * Cr;  /* (t, ci) rows with real input channels */
+    const int nblk = nt > 1 ? (rows < nt ? rows : nt) : 1;
+    (void)nt;
+#pragma omp parallel for num_threads(nblk) schedule(static) if (nblk > 1)
+    for (int blk = 0; blk < nblk; ++blk) {
+        const int r0 = rows * blk / nblk, r1 = rows * (blk + 1) / nblk;
+        for (int n = 0; n < B; ++n)
+            for (int oh = 0; oh < OH; ++oh)
+                for (int ow = 0; ow < OH; ++ow) {
+                    const float* restrict d = dy + (((long)n * OH + oh) * OH + ow) * Co;
+                    if (blk == 0)
+                        for (int co = 0; co < Co; ++co) gb[co] = gb[co] + d[co];
+                    for (int r = r0; r < r1; ++r) {
+                        const int t = r / Cr, ci = r % Cr;
+                        const int ih = oh * S + t / 3 - 1, iw = ow * S + t % 3 - 1;
+                        if (ih < 0 || ih >= H || iw < 0 || iw >= H) continue;
+                        const float xv = in[(((long)n * H + ih) * H + iw) * Ci + ci];
+                        float* restrict a = acc + ((long)t * Ci + ci) * Co;
+                        for (int co = 0; co < Co; ++co) a[co] = fmaf(d[co], xv, a[co]);
                     }
                 }
-            }
-    for (long i = 0; i < (long)Co * 9 * Ci; ++i) grad[OW[l] + i] = acc[i];
+    }
+    for (int co = 0; co < Co; ++co)
+        for (int t = 0; t < 9; ++t)
+            for (int ci = 0; ci < Ci; ++ci) grad[OW[l] + ((long)co * 9 + t) * Ci + ci] = acc[((long)t * Ci + ci) * Co + co];
     for (int co = 0; co < Co; ++co) grad[OB[l] + co] = gb[co];
 }
 
 /* dx[n][q][ci] = (act[n][q][ci] > 0) ? sum_{t asc valid} sum_{co asc} dy[n][p(q,t)][co] * W[co][t][ci] : 0 */
 static void conv_dgrad(int l, const float* restrict dy, const float* restrict w, const float* restrict act, int B,
-                       float* restrict dx) {
+                       float* restrict dx, int nt) {
     const int H = LH[l], Ci = LCI[l], Co = LCO[l], S = LS[l], OH = H / S;
-    float acc[64];
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int n = 0; n < B; ++n)
         for (int ih = 0; ih < H; ++ih)
             for (int iw = 0; iw < H; ++iw) {
+                float acc[64];
                 for (int ci = 0; ci < Ci; ++ci) acc[ci] = 0.0f;
                 for (int t = 0; t < 9; ++t) {
                     const int kh = t / 3, kw = t % 3;
@@ -218,7 +235,10 @@ static void conv_dgrad(int l, const float* restrict dy, const float* restrict w,
 
 /* global average pool + FC: g[n][c] = (sum_{p asc} a3[n][p][c]) * 2^-6;
  * z[n][k] = (fmaf chain over c asc of g[n][c] * W4[k][c]) + b4[k] */
-static void head_fwd(const float* restrict a3, int B, const float* restrict w, float* restrict g, float* restrict z) {
+static void head_fwd(const float* restrict a3, int B, const float* restrict w, float* restrict g, float* restrict z,
+                     int nt) {
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int n = 0; n < B; ++n) {
         for (int c = 0; c < 128; ++c) {
             float s = 0.0f;
@@ -236,13 +256,13 @@ static void head_fwd(const float* restrict a3, int B, const float* restrict w, f
 float orc_ce_row(const float* z, int y, float* dz, int* am);
 
 static float cnn_step(float* restrict w, float* restrict m, const float* hp, const float* x, const int32_t* y,
-                      Work* wk) {
+                      Work* wk, int nt) {
     const int B = (int)hp[3];
     float z[256 * NCP];
-    conv_fwd(1, x, B, w, wk->a1, wk);
-    conv_fwd(2, wk->a1, B, w, wk->a2, wk);
-    conv_fwd(3, wk->a2, B, w, wk->a3, wk);
-    head_fwd(wk->a3, B, w, wk->g, z);
+    conv_fwd(1, x, B, w, wk->a1, wk, nt);
+    conv_fwd(2, wk->a1, B, w, wk->a2, wk, nt);
+    conv_fwd(3, wk->a2, B, w, wk->a3, wk, nt);
+    head_fwd(wk->a3, B, w, wk->g, z, nt);
     float lsum = 0.0f;
     const float fb = (float)B;
     for (int n = 0; n < B; ++n) {
@@ -276,13 +296,14 @@ static float cnn_step(float* restrict w, float* restrict m, const float* hp, con
                 const long i = ((long)n * 64 + p) * 128 + c;
                 wk->d3[i] = wk->a3[i] > 0.0f ? wk->dg[n * 128 + c] : 0.0f;
             }
-    conv_wgrad(3, wk->a2, wk->d3, B, wk->grad, wk);
-    conv_dgrad(3, wk->d3, w, wk->a2, B, wk->d2);
-    conv_wgrad(2, wk->a1, wk->d2, B, wk->grad, wk);
-    conv_dgrad(2, wk->d2, w, wk->a1, B, wk->d1);
-    conv_wgrad(1, x, wk->d1, B, wk->grad, wk);
+    conv_wgrad(3, wk->a2, wk->d3, B, wk->grad, wk, nt);
+    conv_dgrad(3, wk->d3, w, wk->a2, B, wk->d2, nt);
+    conv_wgrad(2, wk->a1, wk->d2, B, wk->grad, wk, nt);
+    conv_dgrad(2, wk->d2, w, wk->a1, B, wk->d1, nt);
+    conv_wgrad(1, x, wk->d1, B, wk->grad, wk, nt);
     /* K5 (same rule as the MLP) */
     const float nlr = -hp[0], mu = hp[1], wd = hp[2];
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (long i = 0; i < P_ALLOC; ++i) {
         const float mv = fmaf(mu, m[i], fmaf(wd, w[i], wk->grad[i]));
         m[i] = mv;
@@ -292,13 +313,14 @@ static float cnn_step(float* restrict w, float* restrict m, const float* hp, con
 }
 
 static int cnn_train_slot(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows,
-                          int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, Work* wk) {
+                          int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, Work* wk,
+                          int nt) {
     for (int i = 0; i < n_steps; ++i) {
         const int64_t s = *step;
         if (s < 0 || s >= hp_rows) return 1;
         const float* row = hp + s * 4;
         const long off = (long)(*offset & (int64_t)(n_train - 1));
-        const float l = cnn_step(w, m, row, x + off * SAMPLE, y + off, wk);
+        const float l = cnn_step(w, m, row, x + off * SAMPLE, y + off, wk, nt);
         if (loss_hist) loss_hist[s] = l;
         *step = s + 1;
         *offset += (int64_t)row[3];
@@ -310,7 +332,17 @@ int orc_cnn_train(float* w, float* m, int64_t* step, int64_t* offset, const floa
                   const float* x, const int32_t* y, int n_train, float* loss_hist) {
     Work* wk = (Work*)malloc(sizeof(Work));
     if (!wk) return 2;
-    const int rc = cnn_train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk);
+    const int rc = cnn_train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk, 1);
+    free(wk);
+    return rc;
+}
+
+int orc_cnn_train_mt(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows,
+                     int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, int threads) {
+    Work* wk = (Work*)malloc(sizeof(Work));
+    if (!wk) return 2;
+    const int rc = cnn_train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk,
+                                  threads > 1 ? threads : 1);
     free(wk);
     return rc;
 }
@@ -329,7 +361,7 @@ int orc_cnn_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t
 #pragma omp for schedule(dynamic, 1)
         for (int s = 0; s < n_slots; ++s)
             rc |= wk ? cnn_train_slot(w[s], m[s], &step[s], &offset[s], hp[s], hp_rows, n_steps, x, y, n_train,
-                                      loss_hist ? loss_hist[s] : NULL, wk)
+                                      loss_hist ? loss_hist[s] : NULL, wk, 1)
                      : 2;
         free(wk);
     }
@@ -337,7 +369,14 @@ int orc_cnn_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t
 }
 
 /* ---- eval (same reduction as the MLP: DESIGN.md §3.5) ------------------------------------- */
+void orc_cnn_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int nt);
+
 void orc_cnn_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out) {
+    orc_cnn_eval_mt(w, vx, vy, n_val, out, 1);
+}
+
+void orc_cnn_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int nt) {
+    if (nt < 1) nt = 1;
     Work* wk = (Work*)malloc(sizeof(Work));
     float* loss = (float*)malloc(sizeof(float) * (size_t)n_val);
     float z[256 * NCP];
@@ -345,10 +384,10 @@ void orc_cnn_eval(const float* w, const float* vx, const int32_t* vy, int n_val,
     for (int r0 = 0; r0 < n_val; r0 += 256) {
         const int B = n_val - r0 < 256 ? n_val - r0 : 256;
         const float* xb = vx + (long)r0 * SAMPLE;
-        conv_fwd(1, xb, B, w, wk->a1, wk);
-        conv_fwd(2, wk->a1, B, w, wk->a2, wk);
-        conv_fwd(3, wk->a2, B, w, wk->a3, wk);
-        head_fwd(wk->a3, B, w, wk->g, z);
+        conv_fwd(1, xb, B, w, wk->a1, wk, nt);
+        conv_fwd(2, wk->a1, B, w, wk->a2, wk, nt);
+        conv_fwd(3, wk->a2, B, w, wk->a3, wk, nt);
+        head_fwd(wk->a3, B, w, wk->g, z, nt);
         for (int n = 0; n < B; ++n) {
             int am = 0;
             loss[r0 + n] = orc_ce_row(z + n * NCP, vy[r0 + n], NULL, &am);
@@ -372,14 +411,14 @@ void orc_cnn_eval(const float* w, const float* vx, const int32_t* vy, int n_val,
 /* Test hooks: single-layer pieces on caller buffers (B samples), for the GPU kernel tests. */
 void orc_cnn_conv_fwd(int l, const float* in, int B, const float* w, float* out) {
     Work* wk = (Work*)malloc(sizeof(Work));
-    conv_fwd(l, in, B, w, out, wk);
+    conv_fwd(l, in, B, w, out, wk, 1);
     free(wk);
 }
 void orc_cnn_conv_wgrad(int l, const float* in, const float* dy, int B, float* grad) {
     Work* wk = (Work*)malloc(sizeof(Work));
-    conv_wgrad(l, in, dy, B, grad, wk);
+    conv_wgrad(l, in, dy, B, grad, wk, 1);
     free(wk);
 }
 void orc_cnn_conv_dgrad(int l, const float* dy, const float* w, const float* act, int B, float* dx) {
-    conv_dgrad(l, dy, w, act, B, dx);
+    conv_dgrad(l, dy, w, act, B, dx, 1);
 }

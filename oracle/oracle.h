@@ -34,6 +34,11 @@ int orc_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t* of
                    int64_t hp_rows, int n_steps, const float* x, const int32_t* y, int n_train, float** loss_hist,
                    int threads);
 void orc_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out /* val_loss, val_acc */);
+/* The same with every step (eval) split over `threads` OpenMP threads by independent outputs:
+ * bitwise the single-thread result.  Used by the plan-driven CPU executor (oracle/cpu_executor.py). */
+int orc_train_mt(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows, int n_steps,
+                 const float* x, const int32_t* y, int n_train, float* loss_hist, int threads);
+void orc_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int threads);
 
 /* softmax-CE of one row of 10 logits (shared by both models) */
 float orc_ce_row(const float* z, int y, float* dz, int* am);
@@ -49,6 +54,9 @@ int orc_cnn_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t
                        int64_t hp_rows, int n_steps, const float* x, const int32_t* y, int n_train, float** loss_hist,
                        int threads);
 void orc_cnn_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out);
+int orc_cnn_train_mt(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows,
+                     int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, int threads);
+void orc_cnn_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int threads);
 void orc_cnn_conv_fwd(int l, const float* in, int B, const float* w, float* out);
 void orc_cnn_conv_wgrad(int l, const float* in, const float* dy, int B, float* grad);
 void orc_cnn_conv_dgrad(int l, const float* dy, const float* w, const float* act, int B, float* dx);

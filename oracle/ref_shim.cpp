@@ -15,6 +15,7 @@
 //  2. ref_call(json) — a JSON command interface exercising the reference's
 //     public API (hpseq.hpp / plan.hpp).  The product exposes the very same
 //     command interface (smh_call) so tests can compare the two byte for byte.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -73,7 +74,8 @@ HpSequence seq_from_json(const std::string& name, const json& j) {
     s.hp_name = name;
     for (const auto& sj : j) {
         Segment seg;
-        seg.function = detail::function_from_json(sj.at("fn"), name, 1);
+        // "spi": steps per logical iteration of {"epochs": n} values; 1 = plain steps
+        seg.function = detail::function_from_json(sj.at("fn"), name, sj.value("spi", StepCount{1}));
         seg.local_start = sj.value("local_start", StepCount{0});
         seg.duration = sj.at("duration").get<StepCount>();
         s.segments.push_back(std::move(seg));
@@ -235,6 +237,37 @@ json run(const json& cmd) {
         if (cmd.value("roundtrip", false))
             out["roundtrip_signature"] = SearchPlan::from_json(plan.to_json()).signature();
         out["file_name"] = PlanStore::file_name(key);
+        if (cmd.value("values", false)) {
+            // the plan as an executable tree for the CPU executor (oracle/cpu_executor.py): each
+            // node's step range [start, hi) and its hp values there, straight from the
+            // reference's SearchPlan::value_at (plan.cpp:278-288)
+            json nv = json::array();
+            for (const PlanNode& n : plan.nodes()) {
+                StepCount hi = n.start_step;
+                json reqs = json::array();
+                for (const auto& e : n.requests) {
+                    hi = std::max(hi, e.end);
+                    json subs = json::array();
+                    for (const auto& t : e.subscribers) subs.push_back({t.study, t.trial});
+                    reqs.push_back({{"id", e.id}, {"end", e.end}, {"subscribers", subs}});
+                }
+                json kids = json::array();
+                for (NodeId c : n.children) {
+                    hi = std::max(hi, plan.node(c).start_step);
+                    kids.push_back(c);
+                }
+                json hps = json::object();
+                for (const auto& h : key.hp_set) {
+                    json v = json::array();
+                    for (StepCount s = n.start_step; s < hi; ++s) v.push_back(plan.value_at(n.id, h, s));
+                    hps[h] = v;
+                }
+                nv.push_back({{"id", n.id}, {"parent", n.parent ? json(*n.parent) : json(nullptr)},
+                              {"start", n.start_step}, {"hi", hi}, {"children", kids}, {"requests", reqs},
+                              {"hps", hps}});
+            }
+            out["node_values"] = nv;
+        }
     } else {
         throw ConfigError("unknown op " + op);
     }

@@ -173,9 +173,14 @@ typedef struct {
 } Work;
 
 /* out[r][n] = epi(sum_k a[r][k] * wt[k][n]) ; wt is W transposed ([K][N]) */
+/* nt > 1 (here and below): independent outputs split over OpenMP threads, every output still one
+ * sequential chain -- bitwise the nt == 1 result (tested). */
 static void fwd_layer(const float* restrict a, int B, int K, const float* restrict wt, int N,
-                      const float* restrict bias, int relu, float* restrict out, float* restrict acc) {
+                      const float* restrict bias, int relu, float* restrict out, int nt) {
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int r = 0; r < B; ++r) {
+        float acc[HID > NCP ? HID : NCP];
         for (int n = 0; n < N; ++n) acc[n] = 0.0f;
         for (int k = 0; k < K; ++k) {
             const float av = a[(long)r * K + k];
@@ -197,8 +202,11 @@ static void transpose(const float* restrict w, int rows, int cols, float* restri
 
 /* gw[o][k] = sum_r dy[r][o] * a[r][k] ; gb[o] = sum_r dy[r][o]  (r ascending) */
 static void wgrad(const float* restrict dy, int ldy, int O, const float* restrict a, int K, int B,
-                  float* restrict gw, float* restrict gb, float* restrict acc) {
+                  float* restrict gw, float* restrict gb, int nt) {
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int o = 0; o < O; ++o) {
+        float acc[D0];
         for (int k = 0; k < K; ++k) acc[k] = 0.0f;
         float sb = 0.0f;
         for (int r = 0; r < B; ++r) {
@@ -214,8 +222,11 @@ static void wgrad(const float* restrict dy, int ldy, int O, const float* restric
 
 /* dx[r][k] = (act[r][k] > 0) ? sum_o dy[r][o] * w[o][k] : 0   (o ascending) */
 static void dgrad(const float* restrict dy, int ldy, int O, const float* restrict w, int K, int B,
-                  const float* restrict act, float* restrict dx, float* restrict acc) {
+                  const float* restrict act, float* restrict dx, int nt) {
+    (void)nt;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (int r = 0; r < B; ++r) {
+        float acc[HID];
         for (int k = 0; k < K; ++k) acc[k] = 0.0f;
         for (int o = 0; o < O; ++o) {
             const float d = dy[(long)r * ldy + o];
@@ -227,15 +238,15 @@ static void dgrad(const float* restrict dy, int ldy, int O, const float* restric
 }
 
 static float train_step(float* restrict w, float* restrict m, const float* hp, const float* x, const int32_t* y,
-                        Work* wk) {
+                        Work* wk, int nt) {
     const int B = (int)hp[3];
     /* forward */
     transpose(w + O_W1, HID, D0, wk->wt1);
     transpose(w + O_W2, HID, HID, wk->wt2);
     transpose(w + O_W3, NCP, HID, wk->wt3);
-    fwd_layer(x, B, D0, wk->wt1, HID, w + O_B1, 1, wk->h1, wk->acc);
-    fwd_layer(wk->h1, B, HID, wk->wt2, HID, w + O_B2, 1, wk->h2, wk->acc);
-    fwd_layer(wk->h2, B, HID, wk->wt3, NCP, w + O_B3, 0, wk->z, wk->acc);
+    fwd_layer(x, B, D0, wk->wt1, HID, w + O_B1, 1, wk->h1, nt);
+    fwd_layer(wk->h1, B, HID, wk->wt2, HID, w + O_B2, 1, wk->h2, nt);
+    fwd_layer(wk->h2, B, HID, wk->wt3, NCP, w + O_B3, 0, wk->z, nt);
     /* loss */
     float lsum = 0.0f;
     const float fb = (float)B;
@@ -247,14 +258,15 @@ static float train_step(float* restrict w, float* restrict m, const float* hp, c
     }
     /* backward */
     memset(wk->g, 0, sizeof wk->g);
-    wgrad(wk->dz, NCP, NCP, wk->h2, HID, B, wk->g + O_W3, wk->g + O_B3, wk->acc);
-    dgrad(wk->dz, NCP, NCP, w + O_W3, HID, B, wk->h2, wk->dh2, wk->acc);
-    wgrad(wk->dh2, HID, HID, wk->h1, HID, B, wk->g + O_W2, wk->g + O_B2, wk->acc);
-    dgrad(wk->dh2, HID, HID, w + O_W2, HID, B, wk->h1, wk->dh1, wk->acc);
-    wgrad(wk->dh1, HID, HID, x, D0, B, wk->g + O_W1, wk->g + O_B1, wk->acc);
+    wgrad(wk->dz, NCP, NCP, wk->h2, HID, B, wk->g + O_W3, wk->g + O_B3, nt);
+    dgrad(wk->dz, NCP, NCP, w + O_W3, HID, B, wk->h2, wk->dh2, nt);
+    wgrad(wk->dh2, HID, HID, wk->h1, HID, B, wk->g + O_W2, wk->g + O_B2, nt);
+    dgrad(wk->dh2, HID, HID, w + O_W2, HID, B, wk->h1, wk->dh1, nt);
+    wgrad(wk->dh1, HID, HID, x, D0, B, wk->g + O_W1, wk->g + O_B1, nt);
     /* K5: g' = fma(wd, w, g); m = fma(mu, m, g'); w = fma(-lr, m, w) */
     const float nlr = -hp[0], mu = hp[1], wd = hp[2];
     const float* restrict g = wk->g;
+#pragma omp parallel for num_threads(nt) schedule(static) if (nt > 1)
     for (long i = 0; i < P_ALLOC; ++i) {
         const float mv = fmaf(mu, m[i], fmaf(wd, w[i], g[i]));
         m[i] = mv;
@@ -264,13 +276,13 @@ static float train_step(float* restrict w, float* restrict m, const float* hp, c
 }
 
 static int train_slot(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows,
-                      int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, Work* wk) {
+                      int n_steps, const float* x, const int32_t* y, int n_train, float* loss_hist, Work* wk, int nt) {
     for (int i = 0; i < n_steps; ++i) {
         const int64_t s = *step;
         if (s < 0 || s >= hp_rows) return 1;
         const float* row = hp + s * 4;
         const long off = (long)(*offset & (int64_t)(n_train - 1));
-        const float l = train_step(w, m, row, x + off * D0, y + off, wk);
+        const float l = train_step(w, m, row, x + off * D0, y + off, wk, nt);
         if (loss_hist) loss_hist[s] = l;
         *step = s + 1;
         *offset += (int64_t)row[3];
@@ -282,7 +294,17 @@ int orc_train(float* w, float* m, int64_t* step, int64_t* offset, const float* h
               const float* x, const int32_t* y, int n_train, float* loss_hist) {
     Work* wk = (Work*)malloc(sizeof(Work));
     if (!wk) return 2;
-    const int rc = train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk);
+    const int rc = train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk, 1);
+    free(wk);
+    return rc;
+}
+
+int orc_train_mt(float* w, float* m, int64_t* step, int64_t* offset, const float* hp, int64_t hp_rows, int n_steps,
+                 const float* x, const int32_t* y, int n_train, float* loss_hist, int threads) {
+    Work* wk = (Work*)malloc(sizeof(Work));
+    if (!wk) return 2;
+    const int rc = train_slot(w, m, step, offset, hp, hp_rows, n_steps, x, y, n_train, loss_hist, wk,
+                              threads > 1 ? threads : 1);
     free(wk);
     return rc;
 }
@@ -301,7 +323,7 @@ int orc_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t* of
 #pragma omp for schedule(dynamic, 1)
         for (int s = 0; s < n_slots; ++s)
             rc |= wk ? train_slot(w[s], m[s], &step[s], &offset[s], hp[s], hp_rows, n_steps, x, y, n_train,
-                                  loss_hist ? loss_hist[s] : NULL, wk)
+                                  loss_hist ? loss_hist[s] : NULL, wk, 1)
                      : 2;
         free(wk);
     }
@@ -309,7 +331,14 @@ int orc_train_many(int n_slots, float** w, float** m, int64_t* step, int64_t* of
 }
 
 /* ---- eval ----------------------------------------------------------- */
+void orc_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int nt);
+
 void orc_eval(const float* w, const float* vx, const int32_t* vy, int n_val, double* out) {
+    orc_eval_mt(w, vx, vy, n_val, out, 1);
+}
+
+void orc_eval_mt(const float* w, const float* vx, const int32_t* vy, int n_val, double* out, int nt) {
+    if (nt < 1) nt = 1;
     Work* wk = (Work*)malloc(sizeof(Work));
     float* loss = (float*)malloc(sizeof(float) * (size_t)n_val);
     transpose(w + O_W1, HID, D0, wk->wt1);
@@ -318,9 +347,9 @@ void orc_eval(const float* w, const float* vx, const int32_t* vy, int n_val, dou
     long correct = 0;
     for (int r0 = 0; r0 < n_val; r0 += MAXB) {
         const int B = n_val - r0 < MAXB ? n_val - r0 : MAXB;
-        fwd_layer(vx + (long)r0 * D0, B, D0, wk->wt1, HID, w + O_B1, 1, wk->h1, wk->acc);
-        fwd_layer(wk->h1, B, HID, wk->wt2, HID, w + O_B2, 1, wk->h2, wk->acc);
-        fwd_layer(wk->h2, B, HID, wk->wt3, NCP, w + O_B3, 0, wk->z, wk->acc);
+        fwd_layer(vx + (long)r0 * D0, B, D0, wk->wt1, HID, w + O_B1, 1, wk->h1, nt);
+        fwd_layer(wk->h1, B, HID, wk->wt2, HID, w + O_B2, 1, wk->h2, nt);
+        fwd_layer(wk->h2, B, HID, wk->wt3, NCP, w + O_B3, 0, wk->z, nt);
         for (int r = 0; r < B; ++r) {
             int am = 0;
             loss[r0 + r] = ce_row(wk->z + (long)r * NCP, vy[r0 + r], NULL, &am);

@@ -833,6 +833,20 @@ int smx_dataset_upload(smx_ctx* c, const float* x, const int32_t* y, const float
     });
 }
 
+int smx_dataset_read(smx_ctx* c, float* x, int32_t* y, float* vx, int32_t* vy) {
+    return guard([&] {
+        if (!x || !y || !vx || !vy) fail(SMX_ECONFIG, "null dataset buffer");
+        cudaSetDevice(c->device);
+        const long long rows = (long long)c->d.n_train + c->d.max_batch;
+        ck(cudaMemcpyAsync(x, c->xtrain, sizeof(float) * rows * c->d_in, cudaMemcpyDeviceToHost, c->stream), "x D2H");
+        ck(cudaMemcpyAsync(y, c->ytrain, sizeof(int) * rows, cudaMemcpyDeviceToHost, c->stream), "y D2H");
+        ck(cudaMemcpyAsync(vx, c->xval, sizeof(float) * (long long)c->d.n_val * c->d_in, cudaMemcpyDeviceToHost, c->stream),
+           "vx D2H");
+        ck(cudaMemcpyAsync(vy, c->yval, sizeof(int) * c->d.n_val, cudaMemcpyDeviceToHost, c->stream), "vy D2H");
+        ck(cudaStreamSynchronize(c->stream), "dataset read sync");
+    });
+}
+
 int smx_host_alloc(uint64_t bytes, void** out) {
     return guard([&] { ck(cudaMallocHost(out, bytes), "cudaMallocHost"); });
 }

@@ -24,7 +24,8 @@ MET_COLS = 2
 
 # Every symbol include/smx.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "smx_open", "smx_close", "smx_param_count", "smx_dataset_digest", "smx_dataset_upload", "smx_host_alloc",
+    "smx_open", "smx_close", "smx_param_count", "smx_dataset_digest", "smx_dataset_upload", "smx_dataset_read",
+    "smx_host_alloc",
     "smx_host_free", "smx_hp_upload", "smx_slot_init",
     "smx_slot_load", "smx_slot_save", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
     "smx_slot_write", "smx_ckpt_read", "smx_ckpt_write", "smx_train", "smx_eval", "smx_losses", "smx_sync",
@@ -83,6 +84,7 @@ def load_library() -> ctypes.CDLL:
             "smx_dataset_digest": [P, ctypes.POINTER(ctypes.c_uint64)],
             "smx_hp_upload": [P, I, I64, I64, FP],
             "smx_dataset_upload": [P, FP, P, FP, P],
+            "smx_dataset_read": [P, FP, P, FP, P],
             "smx_host_alloc": [ctypes.c_uint64, ctypes.POINTER(P)],
             "smx_host_free": [P],
             "smx_slot_init": [P, I],
@@ -142,6 +144,8 @@ class Executor:
         self._ctx = ctypes.c_void_p()
         _check(self._lib.smx_open(ctypes.byref(self.desc), device, n_slots, n_ckpts, ctypes.byref(self._ctx)))
         self.n_slots, self.n_ckpts, self.device = n_slots, n_ckpts, device
+        self.n_train, self.n_val, self.max_batch = n_train, n_val, max_batch
+        self.d_in = 32 * 32 * 4 if model == MODEL_CNN else 784
         p, pa = ctypes.c_int64(), ctypes.c_int64()
         _check(self._lib.smx_param_count(self._ctx, ctypes.byref(p), ctypes.byref(pa)))
         self.p_algo, self.p_alloc = p.value, pa.value
@@ -178,6 +182,16 @@ class Executor:
         assert arrs[0].dtype == np.float32 and arrs[1].dtype == np.int32
         _check(self._lib.smx_dataset_upload(self._ctx, _fp(arrs[0]), arrs[1].ctypes.data, _fp(arrs[2]),
                                             arrs[3].ctypes.data))
+
+    def dataset_read(self):
+        """(x, y, vx, vy): host copies of the context's dataset."""
+        rows = self.n_train + self.max_batch
+        x = np.empty((rows, self.d_in), np.float32)
+        y = np.empty(rows, np.int32)
+        vx = np.empty((self.n_val, self.d_in), np.float32)
+        vy = np.empty(self.n_val, np.int32)
+        _check(self._lib.smx_dataset_read(self._ctx, _fp(x), y.ctypes.data, _fp(vx), vy.ctypes.data))
+        return x, y, vx, vy
 
     def hp_upload(self, slot: int, step0: int, rows: np.ndarray) -> None:
         rows = np.ascontiguousarray(rows, dtype=np.float32).reshape(-1, HP_COLS)

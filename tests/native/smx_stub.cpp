@@ -91,6 +91,7 @@ int smx_dataset_digest(smx_ctx*, uint64_t* out) {
     return SMX_OK;
 }
 int smx_dataset_upload(smx_ctx*, const float*, const int32_t*, const float*, const int32_t*) { return SMX_OK; }
+int smx_dataset_read(smx_ctx*, float*, int32_t*, float*, int32_t*) { return SMX_OK; }
 int smx_host_alloc(uint64_t bytes, void** out) {
     *out = std::malloc(bytes);
     return *out ? SMX_OK : err(SMX_EDEVICE, "malloc");

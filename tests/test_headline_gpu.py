@@ -185,3 +185,67 @@ def test_uploaded_gaussian_data_mlp_tc():
         vl, va = e.eval([0])[0]
         ovl, ova = o.eval(ds=d)
         assert abs(vl - ovl) <= 1e-5 * abs(ovl) and abs(va - ova) <= 2 / ol.N_VAL
+
+
+def c2_mini_spec(T=60):
+    """The C2 grid (64 trials: 8 lr step-decays x 8 momentum sequences, bs 128, wd 5e-4) with
+    T = 1200 scaled to 60 steps: every milestone / switch step scaled by 1/20."""
+    import json
+    from pathlib import Path
+
+    spec = json.loads((Path(__file__).resolve().parent.parent / "paper_2006_11972_b200" / "studies" /
+                       "c2_grid.json").read_text())
+    scale = T / spec["max_steps"]
+    spec["name"], spec["max_steps"], spec["eval_interval"] = "c2_mini", T, T // 3
+    for fns in spec["space"].values():
+        for f in fns:
+            if "milestones" in f:
+                f["milestones"] = [int(m * scale) for m in f["milestones"]]
+    return json.dumps(spec)
+
+
+def test_c2_mini_engine_tc_vs_cpu_reference_executor():
+    """(iii) a truncated C2 study (64 trials, T = 60) through host.Engine in tensor-core mode vs
+    the CPU reference executor (oracle/cpu_executor.py: the reference-built plan executed by the
+    fp32 oracle): every trial's eval metrics within tolerance; STAGE == TRIAL bitwise in TC mode."""
+    import sys
+    from pathlib import Path
+
+    from paper_2006_11972_b200 import host
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    import cpu_executor as cx
+
+    spec = c2_mini_spec()
+    opts = dict(slots_per_gpu=64, max_batch=MAXB, n_train=N_TRAIN, n_val=N_VAL, gemm_mode=ex.GEMM_TC)
+    e = host.Engine.for_study(spec, **opts)
+    e.submit_study(spec)
+    e.run()
+    st = e.stats()
+    info = cx.expand_study(spec)
+    plan = cx.reference_plan(info["key"], info["trials"])
+    unique = sum(n["hi"] - n["start"] for n in plan["node_values"])
+    assert st["stage_steps"] == unique and st["trial_steps"] == 64 * 60
+    assert st["locksteps"] == 60  # acceptance 8: the critical path
+    hist = e.histories()
+    # TRIAL mode (every trial unmerged) records bitwise the same metrics
+    et = host.Engine.for_study(spec, trial_mode=True, **opts)
+    et.submit_study(spec)
+    et.run()
+    assert et.histories() == hist
+    # the CPU reference executor on the reference's plan
+    model = cx.Model("cnn", cx.oracle_lib(), n_train=N_TRAIN, max_batch=MAXB, n_val=N_VAL)
+    res = cx.run_plan(plan, model, eval_interval=info["eval_interval"])
+    assert res["complete"] and res["executed"] == unique
+    cpu = cx.trial_histories(plan, res["metrics"])
+    worst_l = worst_a = 0.0
+    for (study, trial), h in hist.items():
+        ref = cpu[(study, trial)]
+        assert [s for s, _, _ in h] == sorted(ref), (trial, h, sorted(ref))
+        for s, vl, va in h:
+            worst_l = max(worst_l, abs(vl - ref[s]["val_loss"]) / abs(ref[s]["val_loss"]))
+            worst_a = max(worst_a, abs(va - ref[s]["val_acc"]))
+    # 60 SGD steps at lr up to 0.1 / mu 0.9 amplify the 3xTF32 ~1e-6 per-step differences
+    # (DESIGN.md §3.6): bound 1e-3 relative on val_loss, 3 of 256 samples on val_acc
+    assert worst_l <= 1e-3 and worst_a <= 3 / N_VAL, (worst_l, worst_a)
+    print(f"c2_mini: worst val_loss rel {worst_l:.2e}, worst val_acc {worst_a:.4f}")
