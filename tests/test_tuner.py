@@ -233,3 +233,79 @@ def test_grid_tuner_done_with_best():
     s = spec(5, {"kind": "grid"}, max_steps=50)
     acts, win = simulate(s, lambda t, e: abs(t - 3))
     assert acts[:5] == [f"SUBMIT {t} 50" for t in range(5)] and win == [3]
+
+
+# ---------------------------------------------------------------- acceptance 7
+
+def simulate_seeded(spec_json, metric, rng):
+    """Like simulate(), but the next completion is a seeded random pick among in-flight jobs."""
+    t = host.Tuner(spec_json)
+    log, inflight = [], []
+
+    def take(acts):
+        for a in acts:
+            log.append(a)
+            parts = a.split()
+            if parts[0] in ("SUBMIT", "EXTEND"):
+                inflight.append((int(parts[1]), int(parts[2])))
+
+    take(t.start())
+    while inflight:
+        tr, end = inflight.pop(rng.randrange(len(inflight)))
+        take(t.on_result(tr, end, {"val_loss": metric(tr, end), "val_acc": 0.5}))
+    assert t.done()
+    return log, t.winners()
+
+
+def asha_sequential_reference(n, rungs, eta, par, metric, rng):
+    """The published ASHA rule (Li et al. 2020, Alg. 2) run sequentially: a finishing job is
+    promoted iff it ranks in the top ceil(|rung| / eta) of its rung and the rung still has a
+    promotion left; otherwise the next fresh trial starts.  Completion order drawn from `rng`
+    exactly as simulate_seeded draws it."""
+    acts, inflight, res, promoted = [], [], [dict() for _ in rungs], [0] * len(rungs)
+    nxt = 0
+
+    def launch():
+        nonlocal nxt
+        acts.append(f"SUBMIT {nxt} {rungs[0]}")
+        inflight.append((nxt, rungs[0]))
+        nxt += 1
+
+    while nxt < min(par, n):
+        launch()
+    while inflight:
+        t, end = inflight.pop(rng.randrange(len(inflight)))
+        k = rungs.index(end)
+        res[k][t] = metric(t, end)
+        if k + 1 < len(rungs):
+            quota = math.ceil(len(res[k]) / eta)
+            order = sorted(res[k], key=lambda x: (res[k][x], x))
+            if order.index(t) < quota and promoted[k] < quota:
+                promoted[k] += 1
+                acts.append(f"EXTEND {t} {rungs[k + 1]}")
+                inflight.append((t, rungs[k + 1]))
+                continue
+            acts.append(f"STOP {t}")
+        if nxt < n:
+            launch()
+    best = next(r for r in reversed(res) if r)
+    win = min(best, key=lambda x: (best[x], x))
+    acts.append(f"DONE {win}")
+    return acts, [win]
+
+
+RECORDED = random.Random(2020)
+ASHA_TABLE = {(t, e): round(RECORDED.random(), 3) for t in range(20) for e in (5, 15, 45)}
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_asha_200_completion_orders(seed):
+    """SPEC acceptance 7: a fixed recorded metric table (20 trials, 3 rungs 5 / 15 / 45), 200
+    seeded completion orders: the tuner's asynchronous promotion sequence equals the sequential
+    reference of the ASHA rule for every order."""
+    s = spec(20, {"kind": "asha", "reduction": 3, "min": 5, "max": 45, "parallelism": 6}, max_steps=45)
+    assert host.sha_rungs(s)[0] == [5, 15, 45]
+    acts, win = simulate_seeded(s, lambda t, e: ASHA_TABLE[(t, e)], random.Random(seed))
+    want, wwin = asha_sequential_reference(20, [5, 15, 45], 3, 6, lambda t, e: ASHA_TABLE[(t, e)],
+                                           random.Random(seed))
+    assert acts == want and win == wwin
