@@ -125,6 +125,9 @@ int smx_slot_init(smx_ctx* ctx, int slot);                /* kScratch: seeded in
 int smx_slot_load(smx_ctx* ctx, int slot, int ckpt);      /* LOAD: pool -> slot (HBM copy) */
 int smx_slot_save(smx_ctx* ctx, int slot, int ckpt);      /* SAVE: slot -> pool (HBM copy) */
 int smx_ckpt_free(smx_ctx* ctx, int ckpt);                /* GC: entry becomes empty */
+/* STOP / cancel_trial (reference plan.cpp:204-225): the slot's state is abandoned; it must be
+ * re-initialised (smx_slot_init / _load / _write) before it trains or evaluates again. */
+int smx_release_slot(smx_ctx* ctx, int slot);
 int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt); /* NVLink P2P */
 int smx_slot_state(smx_ctx* ctx, int slot, int64_t* step, int64_t* offset);
 int smx_slot_read(smx_ctx* ctx, int slot, float* w, float* m);  /* p_alloc floats each */

@@ -48,6 +48,26 @@ struct EngineOptions {
     double default_lr = 0.1, default_momentum = 0.9, default_wd = 0.0, default_bs = 128;
     // multi-process partition: this process executes only the root subtrees LPT assigns to `rank`
     int rank = 0, world = 1;
+    // profiled seconds-per-step table (batch size -> microseconds per stage-step); after a node's
+    // first executed stage its entry is stored with SearchPlan::set_runtime and
+    // the scheduler's estimator reads it.  Empty: the bs-proportional cost model.
+    std::map<int, double> step_cost_us;
+    // checkpoint GC (plan.hpp:45 ref_count; policy ours): when the
+    // pool is full, an entry no pending request resumes from and no live (un-STOPped) trial can
+    // be extended from is freed instead of spilled to host memory
+    bool ckpt_gc = true;
+};
+
+/// One event of the execution trace (SPEC.md:436 columns time_us,worker,kind,node,start,end,
+/// detail).  Time is the engine's logical lockstep clock in training steps, so repeated runs
+/// give byte-identical traces (acceptance 10); device time is in EngineStats.
+struct TraceEvent {
+    StepCount time = 0;
+    int worker = 0;
+    std::string kind;  // LOAD, TRAIN, SAVE, EVAL, IDLE
+    NodeId node = -1;
+    StepCount start = 0, end = 0;
+    std::string detail;
 };
 
 struct EngineStats {
@@ -57,6 +77,12 @@ struct EngineStats {
     std::int64_t trial_steps = 0; // sum over trials of the furthest end step reported to them
                                   // (the work TRIAL mode would do; extensions count once)
     std::int64_t saves = 0, loads = 0, inits = 0, peer_copies = 0, evals = 0, assignments = 0, spills = 0;
+    std::int64_t releases = 0;    // in-flight slots freed because STOP cancelled every request they served
+    std::int64_t gc_frees = 0;    // pool entries freed by checkpoint GC (no spill)
+    // the cost model's time of the executed schedule (deterministic, SPEC.md:403/:428 semantics
+    // with zero save/load/eval overheads): busy = sum over workers, wall = per lockstep the
+    // slowest active worker
+    double model_busy_us = 0, model_wall_us = 0;
     std::int64_t kernel_launches = 0;
     std::int64_t h2d_bytes = 0, d2h_bytes = 0;
 };
@@ -73,6 +99,10 @@ public:
 
     /// Inserts a trial into the plan (in TRIAL mode onto its own unmerged path).
     InsertOutcome submit(const TrialRequest& req);
+    /// STOP / cancel_trial (plan.cpp:204-225): drops the trial's pending request; in-flight
+    /// assignments are cut after their last stage that still serves a pending request, and a
+    /// worker left with nothing to serve releases its slot (smx_release_slot).  Shared stages
+    /// keep running.
     bool cancel(const TrialRef& t);
 
     using CompletionFn = std::function<void(Engine&, const CompletedRequest&)>;
@@ -92,6 +122,12 @@ public:
 
     const SearchPlan& plan() const { return *plan_; }
     const EngineStats& stats() const { return stats_; }
+    const std::vector<TraceEvent>& trace() const { return trace_; }
+    /// Frees every checkpoint-pool entry the GC policy considers dead; returns how many.
+    int collect_checkpoints();
+    /// Profiles microseconds per stage-step for each batch size (timed locksteps on idle slots of
+    /// the first GPU, 3 significant digits) into options().step_cost_us.  Needs idle workers.
+    void calibrate(const std::vector<int>& batch_sizes);
     const EngineOptions& options() const { return opts_; }
     MetricHistory history(const TrialRef& t) const;
     std::vector<TrialRef> trials() const;
@@ -112,6 +148,10 @@ private:
     int alloc_entry(int gpu);
     TimeUs est_us(NodeId n) const;
     std::set<NodeId> blocked_nodes() const;
+    void release_orphans();
+    std::set<CkptHandle> needed_checkpoints() const;
+    double step_cost_us(double bs) const;
+    void emit(int worker, const char* kind, NodeId node, StepCount start, StepCount end, std::string detail = {});
 
     CompatKey key_;
     EngineOptions opts_;
@@ -132,6 +172,9 @@ private:
     };
     std::map<CkptHandle, HostCkpt> spilled_;  // host spill tier of the checkpoint pool
     std::uint64_t use_clock_ = 0;
+    std::vector<TraceEvent> trace_;
+    StepCount clock_ = 0;               // logical lockstep clock (training steps)
+    std::set<TrialRef> stopped_;        // trials STOPped / cancelled (never extended again)
     std::int64_t p_alloc_ = 0;
     std::int64_t d_in_ = 784;  // floats per input sample of the model
 };

@@ -38,6 +38,9 @@ EngineOptions options_from(const json& o) {
     e.default_bs = o.value("default_bs", e.default_bs);
     e.rank = o.value("rank", 0);
     e.world = o.value("world", 1);
+    if (o.contains("step_cost_us"))
+        for (const auto& [k, v] : o.at("step_cost_us").items()) e.step_cost_us[std::stoi(k)] = v.get<double>();
+    e.ckpt_gc = o.value("ckpt_gc", e.ckpt_gc);
     return e;
 }
 
@@ -46,7 +49,8 @@ json stats_json(const EngineStats& s) {
             {"trial_steps", s.trial_steps}, {"saves", s.saves},       {"loads", s.loads},
             {"inits", s.inits},           {"peer_copies", s.peer_copies}, {"evals", s.evals},
             {"assignments", s.assignments}, {"spills", s.spills},     {"kernel_launches", s.kernel_launches},
-            {"h2d_bytes", s.h2d_bytes},   {"d2h_bytes", s.d2h_bytes}};
+            {"h2d_bytes", s.h2d_bytes},   {"d2h_bytes", s.d2h_bytes},   {"releases", s.releases},
+            {"gc_frees", s.gc_frees},     {"model_busy_us", s.model_busy_us}, {"model_wall_us", s.model_wall_us}};
 }
 
 template <class F>
@@ -112,6 +116,34 @@ void bind_engine(py::module_& m) {
                  translate([&] { e.run(); });
              })
         .def("reset", [](Engine& e) { translate([&] { e.reset(); }); })
+        .def("trace",
+             [](Engine& e) {
+                 std::vector<std::tuple<long long, int, std::string, long long, long long, long long, std::string>> v;
+                 for (const TraceEvent& t : e.trace()) v.emplace_back(t.time, t.worker, t.kind, t.node, t.start, t.end, t.detail);
+                 return v;
+             })
+        .def("on_complete",
+             [](Engine& e, py::object fn) {
+                 if (fn.is_none()) {
+                     e.on_complete(nullptr);
+                     return;
+                 }
+                 // called from run() (GIL released there): take the GIL for the Python callback
+                 e.on_complete([fn](Engine&, const CompletedRequest& c) {
+                     py::gil_scoped_acquire gil;
+                     std::vector<std::pair<int, int>> subs;
+                     for (const TrialRef& t : c.subscribers) subs.emplace_back(t.study, t.trial);
+                     fn(c.node, c.end, subs);
+                 });
+             })
+        .def("collect_checkpoints", [](Engine& e) { return translate([&] { return e.collect_checkpoints(); }); })
+        .def("calibrate",
+             [](Engine& e, const std::vector<int>& bss) {
+                 py::gil_scoped_release nogil;
+                 translate([&] { e.calibrate(bss); });
+             })
+        .def("step_cost_us", [](Engine& e) { return e.options().step_cost_us; })
+        .def("node_runtime", [](Engine& e, long long n) { return e.plan().node(n).runtime_sec_per_step; })
         .def("stats", [](Engine& e) { return stats_json(e.stats()).dump(); })
         .def("signature", [](Engine& e) { return e.plan().signature(); })
         .def("plan_json", [](Engine& e) { return e.plan().to_json(); })

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -47,6 +48,7 @@ struct Engine::Worker {
     Assignment a;
     std::size_t cur = 0;
     StepCount remaining = 0;
+    double cost_us = 0;  // cost model's us per step of the current stage
 };
 
 Engine::Engine(CompatKey key, EngineOptions opts) : key_(std::move(key)), opts_(std::move(opts)) {
@@ -118,6 +120,13 @@ void Engine::reset() {
     root_owner_.clear();
     stats_ = EngineStats{};
     next_assignment_ = 0;
+    trace_.clear();
+    clock_ = 0;
+    stopped_.clear();
+}
+
+void Engine::emit(int worker, const char* kind, NodeId node, StepCount start, StepCount end, std::string detail) {
+    trace_.push_back(TraceEvent{clock_, worker, kind, node, start, end, std::move(detail)});
 }
 
 void Engine::upload_dataset(const float* x, const std::int32_t* y, const float* vx, const std::int32_t* vy) {
@@ -144,6 +153,7 @@ InsertOutcome Engine::submit(const TrialRequest& in) {
         throw ConfigError("trial longer than the executor's max_steps (" + std::to_string(opts_.max_steps) + ")");
     InsertOutcome out = plan_->insert_trial(req);
     const TrialRef t{in.study, in.trial};
+    stopped_.erase(t);
     trial_index_[t] = {req.config.total_steps, out.node};
     trial_cfg_[t] = in.config;
     if (out.kind == InsertOutcome::Kind::kImmediate) credit(t, req.config.total_steps);
@@ -158,7 +168,111 @@ void Engine::credit(const TrialRef& t, StepCount end) {
     }
 }
 
-bool Engine::cancel(const TrialRef& t) { return plan_->cancel_trial(t); }
+bool Engine::cancel(const TrialRef& t) {
+    stopped_.insert(t);
+    const bool changed = plan_->cancel_trial(t);
+    if (changed) release_orphans();
+    return changed;
+}
+
+void Engine::release_orphans() {
+    std::set<RequestId> live;
+    for (const PendingRequest& p : plan_->pending_requests()) live.insert(p.id);
+    for (auto& w : workers_) {
+        if (!w->busy) continue;
+        // one past the last stage (from the current one) that still serves a pending request
+        std::size_t keep = w->cur;
+        for (std::size_t i = w->a.stages.size(); i-- > w->cur;) {
+            const auto& sv = w->a.stages[i].serves;
+            if (std::any_of(sv.begin(), sv.end(), [&](RequestId r) { return live.count(r) > 0; })) {
+                keep = i + 1;
+                break;
+            }
+        }
+        if (keep == w->cur) {
+            smx_ok(smx_release_slot(gpus_[static_cast<std::size_t>(w->gpu)]->ctx, w->slot), "smx_release_slot");
+            w->busy = false;
+            w->remaining = 0;
+            stats_.releases += 1;
+            emit(w->id, "IDLE", w->a.stages[w->cur].node, w->a.stages[w->cur].start, w->a.stages[w->cur].end,
+                 "released");
+        } else if (keep < w->a.stages.size()) {
+            w->a.stages.resize(keep);
+        }
+    }
+}
+
+std::set<CkptHandle> Engine::needed_checkpoints() const {
+    // what a pending request would resume from now, and what an EXTEND of any live (un-STOPped)
+    // trial would resume from; everything else in the pool is dead
+    std::set<CkptHandle> need;
+    FindCheckpointMemo memo;
+    auto add = [&](NodeId node, StepCount step) {
+        const ResumePoint rp = find_latest_checkpoint(*plan_, node, step, &memo, nullptr);
+        if (rp.kind == ResumeKind::kCheckpoint) need.insert(plan_->node(rp.ckpt.node).ckpts.at(rp.ckpt.step));
+    };
+    for (const PendingRequest& p : plan_->pending_requests()) add(p.node, p.end);
+    for (const auto& [t, ent] : trial_index_)
+        if (!stopped_.count(t)) add(ent.second, ent.first);
+    return need;
+}
+
+int Engine::collect_checkpoints() {
+    const std::set<CkptHandle> need = needed_checkpoints();
+    int freed = 0;
+    for (auto& gp : gpus_) {
+        Gpu& g = *gp;
+        for (int e = 0; e < opts_.ckpts_per_gpu; ++e) {
+            const CkptHandle& h = g.handle_of[static_cast<std::size_t>(e)];
+            if (h.empty() || need.count(h)) continue;
+            g.entry_of.erase(h);
+            g.handle_of[static_cast<std::size_t>(e)].clear();
+            smx_ok(smx_ckpt_free(g.ctx, e), "smx_ckpt_free");
+            g.free_entries.push_back(e);
+            ++freed;
+        }
+    }
+    for (auto it = spilled_.begin(); it != spilled_.end();)
+        it = need.count(it->first) ? std::next(it) : spilled_.erase(it);
+    stats_.gc_frees += freed;
+    return freed;
+}
+
+double Engine::step_cost_us(double bs) const {
+    if (const auto it = opts_.step_cost_us.find(static_cast<int>(bs)); it != opts_.step_cost_us.end()) return it->second;
+    return bs;  // cost model: proportional to the batch size
+}
+
+void Engine::calibrate(const std::vector<int>& batch_sizes) {
+    for (auto& w : workers_)
+        if (w->busy) throw IntegrityError("calibrate while workers are busy");
+    smx_ctx* ctx = gpus_.front()->ctx;
+    const int k = std::min(opts_.slots_per_gpu, 64);
+    std::vector<int> slots(static_cast<std::size_t>(k));
+    std::iota(slots.begin(), slots.end(), 0);
+    for (int bs : batch_sizes) {
+        if (bs < 1 || bs > opts_.max_batch) throw ConfigError("calibrate: batch size outside [1, max_batch]");
+        std::vector<float> rows;
+        for (int i = 0; i < 4; ++i) rows.insert(rows.end(), {0.01f, 0.9f, 0.0f, static_cast<float>(bs)});
+        for (int sl : slots) {
+            smx_ok(smx_slot_init(ctx, sl), "smx_slot_init");
+            smx_ok(smx_hp_upload(ctx, sl, 0, 4, rows.data()), "smx_hp_upload");
+        }
+        smx_ok(smx_set_timing(ctx, 1), "smx_set_timing");
+        smx_ok(smx_train(ctx, k, slots.data(), 1), "smx_train");
+        smx_stats a{}, b{};
+        smx_get_stats(ctx, &a);
+        smx_ok(smx_train(ctx, k, slots.data(), 3), "smx_train");
+        smx_get_stats(ctx, &b);
+        smx_ok(smx_set_timing(ctx, 0), "smx_set_timing");
+        const double us = (b.lockstep_ms - a.lockstep_ms) * 1e3 / (3.0 * k);
+        const double mag = std::pow(10.0, std::floor(std::log10(std::max(us, 1e-9))) - 2);
+        opts_.step_cost_us[bs] = std::round(us / mag) * mag;  // 3 significant digits
+        for (int sl : slots) smx_ok(smx_release_slot(ctx, sl), "smx_release_slot");
+    }
+    smx_ok(smx_sync(ctx), "smx_sync");
+    smx_reset_stats(ctx);
+}
 
 std::vector<TrialRef> Engine::trials() const {
     std::vector<TrialRef> v;
@@ -182,11 +296,15 @@ MetricHistory Engine::history(const TrialRef& t) const {
 }
 
 TimeUs Engine::est_us(NodeId n) const {
-    // deterministic cost model: proportional to the batch size at the node's start
-    const auto& cfg = plan_->node(n).config;
+    // StepTimeEstimator (stage_tree.hpp:88-90): the node's stored runtime once a stage of it ran
+    // (SearchPlan::set_runtime), else the profile table / bs-proportional model at
+    // the batch size of the node's start -- a pure function of the plan, so schedules are
+    // deterministic
+    const PlanNode& node = plan_->node(n);
+    if (node.runtime_sec_per_step > 0) return std::max<TimeUs>(1, std::llround(node.runtime_sec_per_step * 1e6));
     double bs = opts_.default_bs;
-    if (cfg.count(opts_.hp_bs)) bs = plan_->value_at(n, opts_.hp_bs, plan_->node(n).start_step);
-    return std::max<TimeUs>(1, static_cast<TimeUs>(bs));
+    if (node.config.count(opts_.hp_bs)) bs = plan_->value_at(n, opts_.hp_bs, node.start_step);
+    return std::max<TimeUs>(1, std::llround(step_cost_us(bs)));
 }
 
 std::set<NodeId> Engine::owned_roots() const {
@@ -214,9 +332,25 @@ std::set<NodeId> Engine::blocked_nodes() const {
 
 int Engine::alloc_entry(int gpu) {
     Gpu& g = *gpus_[static_cast<std::size_t>(gpu)];
+    if (g.free_entries.empty() && opts_.ckpt_gc) {
+        // pool full: free the least recently used dead entry (checkpoint GC, no spill)
+        const std::set<CkptHandle> need = needed_checkpoints();
+        int victim = -1;
+        for (int e = 0; e < opts_.ckpts_per_gpu; ++e)
+            if (!need.count(g.handle_of[static_cast<std::size_t>(e)]) &&
+                (victim < 0 || g.last_use[static_cast<std::size_t>(e)] < g.last_use[static_cast<std::size_t>(victim)]))
+                victim = e;
+        if (victim >= 0) {
+            g.entry_of.erase(g.handle_of[static_cast<std::size_t>(victim)]);
+            g.handle_of[static_cast<std::size_t>(victim)].clear();
+            smx_ok(smx_ckpt_free(g.ctx, victim), "smx_ckpt_free");
+            g.free_entries.push_back(victim);
+            stats_.gc_frees += 1;
+        }
+    }
     if (g.free_entries.empty()) {
-        // pool full: spill the least recently used entry to host memory (the checkpoint spill
-        // tier); a later LOAD brings it back with smx_ckpt_write
+        // every entry is still needed: spill the least recently used one to host memory (the
+        // checkpoint spill tier); a later LOAD brings it back with smx_ckpt_write
         int victim = -1;
         for (int e = 0; e < opts_.ckpts_per_gpu; ++e)
             if (victim < 0 || g.last_use[static_cast<std::size_t>(e)] < g.last_use[static_cast<std::size_t>(victim)])
@@ -293,6 +427,9 @@ void Engine::begin_stage(Worker& w) {
     const Stage& s = w.a.stages[w.cur];
     upload_hp(w, s);
     w.remaining = s.end - s.start;
+    const PlanNode& n = plan_->node(s.node);
+    w.cost_us = step_cost_us(n.config.count(opts_.hp_bs) ? plan_->value_at(s.node, opts_.hp_bs, s.start) : opts_.default_bs);
+    if (s.end > s.start) emit(w.id, "TRAIN", s.node, s.start, s.end);
 }
 
 void Engine::start(const Assignment& a) {
@@ -311,10 +448,12 @@ void Engine::start(const Assignment& a) {
         if (e < 0) throw IntegrityError("checkpoint " + it->second + " is not resident on any GPU");
         smx_ok(smx_slot_load(ctx, w.slot, e), "smx_slot_load");
         stats_.loads += 1;
+        emit(w.id, "LOAD", first.resume->node, first.resume->step, first.resume->step, it->second);
     } else {
         if (first.start != 0) throw IntegrityError("scratch stage must start at step 0");
         smx_ok(smx_slot_init(ctx, w.slot), "smx_slot_init");
         stats_.inits += 1;
+        emit(w.id, "LOAD", first.node, 0, 0, "init");
     }
     stats_.assignments += 1;
     begin_stage(w);
@@ -341,19 +480,24 @@ void Engine::finish_stages(std::vector<Worker*>& done) {
         const CkptHandle h = hex16(plan_->prefix_digest_at(s.node, s.end));
         const PlanNode& n = plan_->node(s.node);
         Gpu& g = *gpus_[static_cast<std::size_t>(w->gpu)];
-        if (!n.ckpts.count(s.end) || !g.entry_of.count(h)) {
-            bool resident = false;
-            for (const auto& og : gpus_) resident = resident || og->entry_of.count(h);
-            resident = resident || spilled_.count(h);
-            if (!resident) {
-                const int e = alloc_entry(w->gpu);
-                smx_ok(smx_slot_save(g.ctx, w->slot, e), "smx_slot_save");
-                g.entry_of[h] = e;
-                g.handle_of[static_cast<std::size_t>(e)] = h;
-                stats_.saves += 1;
-            }
+        bool resident = false;
+        for (const auto& og : gpus_) resident = resident || og->entry_of.count(h);
+        resident = resident || spilled_.count(h);
+        if (!resident) {
+            const int e = alloc_entry(w->gpu);
+            smx_ok(smx_slot_save(g.ctx, w->slot, e), "smx_slot_save");
+            g.entry_of[h] = e;
+            g.handle_of[static_cast<std::size_t>(e)] = h;
+            stats_.saves += 1;
         }
+        emit(w->id, "SAVE", s.node, s.end, s.end, resident ? "resident:" + h : h);
         plan_->record_checkpoint(s.node, s.end, h);
+        // the node's runtime after its first executed stage: the profiled cost
+        // of its batch size (SearchPlan::set_runtime, plan.cpp:290-292)
+        if (n.runtime_sec_per_step <= 0) {
+            const double bs = n.config.count(opts_.hp_bs) ? plan_->value_at(s.node, opts_.hp_bs, s.start) : opts_.default_bs;
+            plan_->set_runtime(s.node, step_cost_us(bs) * 1e-6);
+        }
     }
     // EVAL, batched per GPU
     std::map<int, std::vector<Worker*>> by_gpu;
@@ -374,18 +518,32 @@ void Engine::finish_stages(std::vector<Worker*>& done) {
     }
     // aggregate: record metrics, fan out completions, advance workers (ascending id)
     for (Worker* w : done) {
+        if (!w->busy) continue;  // released by a STOP issued from an earlier completion callback
         const Stage s = w->a.stages[w->cur];
         if (auto it = records.find(w->id); it != records.end()) {
-            for (const CompletedRequest& c : plan_->record_metrics(s.node, s.end, it->second)) {
+            const std::vector<CompletedRequest> comp = plan_->record_metrics(s.node, s.end, it->second);
+            char buf[96];
+            std::snprintf(buf, sizeof buf, "val_acc=%.17g;val_loss=%.17g", it->second.at("val_acc"),
+                          it->second.at("val_loss"));
+            std::string detail = buf;
+            std::string who;
+            for (const CompletedRequest& c : comp)
+                for (const TrialRef& t : c.subscribers) who += (who.empty() ? "" : ",") + std::to_string(t.study) + ":" + std::to_string(t.trial);
+            if (!who.empty()) detail += ";trials=" + who;
+            emit(w->id, "EVAL", s.node, s.end, s.end, detail);
+            for (const CompletedRequest& c : comp) {
                 for (const TrialRef& t : c.subscribers) credit(t, c.end);
                 if (on_complete_) on_complete_(*this, c);
             }
         }
+        if (!w->busy) continue;  // this worker's own remaining path was released by the callback
         w->cur += 1;
-        if (w->cur < w->a.stages.size())
+        if (w->cur < w->a.stages.size()) {
             begin_stage(*w);
-        else
+        } else {
             w->busy = false;
+            emit(w->id, "IDLE", s.node, s.end, s.end);
+        }
     }
 }
 
@@ -422,8 +580,16 @@ void Engine::run() {
                    "smx_train");
             stats_.locksteps += k;
         }
-        for (Worker* w : active) w->remaining -= k;
+        double busy = 0, slowest = 0;
+        for (Worker* w : active) {
+            w->remaining -= k;
+            busy += w->cost_us;
+            slowest = std::max(slowest, w->cost_us);
+        }
+        stats_.model_busy_us += busy * static_cast<double>(k);
+        stats_.model_wall_us += slowest * static_cast<double>(k);
         stats_.stage_steps += k * static_cast<StepCount>(active.size());
+        clock_ += k;
     }
     for (auto& g : gpus_) smx_ok(smx_sync(g->ctx), "smx_sync");
     std::int64_t launches = 0;

@@ -76,6 +76,7 @@ struct smx_ctx {
     CopyJob* jobs = nullptr;    // device job list for fork copies
     int jobs_cap = 0;
     std::vector<char> ck_valid;
+    std::vector<char> slot_live;  // slot holds a state (init / load / write since open or release)
     // every training / validation input value is exact in tf32 (true for the synthetic k/128
     // data; re-checked on every smx_dataset_upload): only then may the tensor-core GEMMs skip
     // the data operand's lo MMA
@@ -738,6 +739,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             ck(cudaMemsetAsync(c->st, 0, sizeof(SlotState) * n_slots, c->stream), "state zero");
             for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
             c->ck_valid.assign(n_ckpts, 0);
+            c->slot_live.assign(n_slots, 0);
             if (c->cnn) make_conv_tmaps(c);
             gen_dataset(c);
             ck(cudaStreamSynchronize(c->stream), "open sync");
@@ -889,6 +891,7 @@ int smx_slot_init(smx_ctx* c, int slot) {
                                                     init_scale(kH));
         launch_check(c, "init");
         ck(cudaMemsetAsync(c->st + slot, 0, sizeof(SlotState), c->stream), "state reset");
+        c->slot_live[slot] = 1;
     });
 }
 
@@ -901,6 +904,7 @@ int smx_slot_load(smx_ctx* c, int slot, int ckpt) {
         CopyJob j{reinterpret_cast<const float4*>(c->pool + c->slab_stride() * ckpt),
                   reinterpret_cast<float4*>(c->slab + c->slab_stride() * slot), c->ck_st + ckpt, c->st + slot};
         run_copy(c, {j});
+        c->slot_live[slot] = 1;
     });
 }
 
@@ -913,6 +917,13 @@ int smx_slot_save(smx_ctx* c, int slot, int ckpt) {
                   reinterpret_cast<float4*>(c->pool + c->slab_stride() * ckpt), c->st + slot, c->ck_st + ckpt};
         run_copy(c, {j});
         c->ck_valid[ckpt] = 1;
+    });
+}
+
+int smx_release_slot(smx_ctx* c, int slot) {
+    return guard([&] {
+        check_slot(c, slot);
+        c->slot_live[slot] = 0;
     });
 }
 
@@ -994,6 +1005,7 @@ int smx_slot_write(smx_ctx* c, int slot, const float* w, const float* m, int64_t
         SlotState s{step, offset};
         ck(cudaMemcpyAsync(c->st + slot, &s, sizeof s, cudaMemcpyHostToDevice, c->stream), "state H2D");
         ck(cudaStreamSynchronize(c->stream), "write sync");
+        c->slot_live[slot] = 1;
     });
 }
 
@@ -1036,6 +1048,7 @@ int smx_train(smx_ctx* c, int n_active, const int* slots, int n_steps) {
         for (int s : v) {
             check_slot(c, s);
             if (seen[s]) fail(SMX_ECONFIG, "slot " + std::to_string(s) + " listed twice");
+            if (!c->slot_live[s]) fail(SMX_ECONFIG, "slot " + std::to_string(s) + " has no state (init / load it first)");
             seen[s] = 1;
         }
         cudaSetDevice(c->device);
@@ -1081,7 +1094,10 @@ int smx_eval(smx_ctx* c, int n, const int* slots, double* out) {
         const long long per = (long long)nv * (2 * kH + kCP);
         for (int base = 0; base < n; base += kEvalChunk) {
             const int k = std::min(kEvalChunk, n - base);
-            for (int i = 0; i < k; ++i) check_slot(c, slots[base + i]);
+            for (int i = 0; i < k; ++i) {
+                check_slot(c, slots[base + i]);
+                if (!c->slot_live[slots[base + i]]) fail(SMX_ECONFIG, "eval of a slot with no state");
+            }
             ck(cudaMemcpyAsync(c->eval_slots, slots + base, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream),
                "eval slots H2D");
             if (c->cnn) {

@@ -27,7 +27,7 @@ EXPORTS = (
     "smx_open", "smx_close", "smx_param_count", "smx_dataset_digest", "smx_dataset_upload", "smx_dataset_read",
     "smx_host_alloc",
     "smx_host_free", "smx_hp_upload", "smx_slot_init",
-    "smx_slot_load", "smx_slot_save", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
+    "smx_slot_load", "smx_slot_save", "smx_release_slot", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
     "smx_slot_write", "smx_ckpt_read", "smx_ckpt_write", "smx_train", "smx_eval", "smx_losses", "smx_sync",
     "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel", "smx_test_gemm",
     "smx_last_error", "smx_version",
@@ -91,6 +91,7 @@ def load_library() -> ctypes.CDLL:
             "smx_slot_load": [P, I, I],
             "smx_slot_save": [P, I, I],
             "smx_ckpt_free": [P, I],
+            "smx_release_slot": [P, I],
             "smx_ckpt_peer_copy": [P, I, P, I],
             "smx_slot_state": [P, I, ctypes.POINTER(I64), ctypes.POINTER(I64)],
             "smx_slot_read": [P, I, FP, FP],
@@ -205,6 +206,9 @@ class Executor:
 
     def slot_save(self, slot: int, ckpt: int) -> None:
         _check(self._lib.smx_slot_save(self._ctx, slot, ckpt))
+
+    def release_slot(self, slot: int) -> None:
+        _check(self._lib.smx_release_slot(self._ctx, slot))
 
     def ckpt_free(self, ckpt: int) -> None:
         _check(self._lib.smx_ckpt_free(self._ctx, ckpt))

@@ -97,6 +97,23 @@ class Engine:
     def stats(self) -> dict:
         return json.loads(self._e.stats())
 
+    def trace(self) -> list:
+        """Execution events (time, worker, kind, node, start, end, detail); time = the logical
+        lockstep clock in steps (deterministic)."""
+        return self._e.trace()
+
+    def collect_checkpoints(self) -> int:
+        return self._e.collect_checkpoints()
+
+    def calibrate(self, batch_sizes) -> dict:
+        """Profile us per stage-step for each batch size into the engine's step-cost table."""
+        self._e.calibrate(list(batch_sizes))
+        return self._e.step_cost_us()
+
+    def on_complete(self, fn) -> None:
+        """fn(node, end, [(study, trial), ...]) on every completed request (may call cancel)."""
+        self._e.on_complete(fn)
+
     def signature(self) -> str:
         return self._e.signature()
 

@@ -136,6 +136,12 @@ int smx_slot_save(smx_ctx* c, int slot, int ckpt) {
     return SMX_OK;
 }
 
+int smx_release_slot(smx_ctx* c, int slot) {
+    if (slot < 0 || slot >= c->S) return err(SMX_ECONFIG, "slot out of range");
+    c->slot[static_cast<size_t>(slot)] = State{-1, 0, 0};  // no state: train / eval fail until init / load
+    return SMX_OK;
+}
+
 int smx_ckpt_free(smx_ctx* c, int ckpt) {
     if (ckpt < 0 || ckpt >= c->C) return err(SMX_ECONFIG, "checkpoint out of range");
     c->ck_valid[static_cast<size_t>(ckpt)] = 0;
@@ -210,6 +216,7 @@ int smx_train(smx_ctx* c, int n_active, const int* slots, int n_steps) {
     for (int k = 0; k < n_steps; ++k)
         for (int i = 0; i < n_active; ++i) {
             State& st = c->slot[static_cast<size_t>(slots[i])];
+            if (st.step < 0) return err(SMX_ECONFIG, "slot has no state");
             if (st.step >= c->d.max_steps) return err(SMX_ECONFIG, "step beyond max_steps");
             const size_t r = static_cast<size_t>(slots[i]) * c->d.max_steps + static_cast<size_t>(st.step);
             if (!c->hp_set[r]) return err(SMX_EINTEGRITY, "no hp row uploaded for slot " + std::to_string(slots[i]) +
@@ -229,6 +236,7 @@ int smx_eval(smx_ctx* c, int n, const int* slots, double* out) {
     for (int i = 0; i < n; ++i) {
         if (slots[i] < 0 || slots[i] >= c->S) return err(SMX_ECONFIG, "slot out of range");
         const State& s = c->slot[static_cast<size_t>(slots[i])];
+        if (s.step < 0) return err(SMX_ECONFIG, "eval of a slot with no state");
         const uint64_t h = mix(s.digest, &s.offset, sizeof s.offset);
         out[i * SMX_MET_COLS + SMX_MET_VAL_LOSS] = static_cast<double>(h >> 11) * 0x1p-53;
         out[i * SMX_MET_COLS + SMX_MET_VAL_ACC] = static_cast<double>(s.step);

@@ -134,3 +134,121 @@ def test_c2_grid_makespan_is_critical_path():
     assert st["stage_steps"] == info["unique_steps"] == 41000
     assert st["trial_steps"] == info["total_steps"] == 76800
     assert st["locksteps"] == 1200, st
+
+
+def lr_trial(lr, steps):
+    return {"total_steps": steps, "hps": {"lr": [{"fn": {"family": "constant", "value": lr}, "local_start": 0,
+                                                  "duration": steps}]}}
+
+
+KEY_LR = {"model": "mlp", "dataset": "synthetic", "hp_set": ["lr"]}
+
+
+def test_stop_releases_in_flight_slot():
+    """STOP of a trial whose only pending request is in flight frees that worker's slot
+    (smx_release_slot); the shared prefix it served for another trial was already trained."""
+    e = engine(KEY_LR, slots_per_gpu=4)
+    for i, (lr, T) in enumerate([("0.1", 20), ("0.1", 300), ("0.01", 300)]):
+        e.submit(json.dumps(lr_trial(lr, T)), i, 0, i)
+    stops = []
+
+    def on_done(node, end, subs):
+        if (0, 0) in [tuple(s) for s in subs]:
+            stops.append(e.cancel(0, 1))
+
+    e.on_complete(on_done)
+    e.run()
+    st = json.loads(e.stats())
+    assert stops == [True] and st["releases"] == 1
+    assert st["stage_steps"] == 20 + 300 and st["locksteps"] == 300
+    assert not e.has_pending()
+    assert [s for s, _, _ in e.history(0, 1)] == [20] and len(e.history(0, 2)) == 1  # never reached 300
+    idle = [ev for ev in e.trace() if ev[2] == "IDLE" and ev[6] == "released"]
+    assert len(idle) == 1 and idle[0][0] == 20
+
+
+def test_stop_keeps_shared_stages_running():
+    """STOP of one of two trials sharing an in-flight path: the other still needs it -> no release."""
+    e = engine(KEY_LR, slots_per_gpu=4)
+    for i, (lr, T) in enumerate([("0.1", 20), ("0.1", 300), ("0.1", 200)]):
+        e.submit(json.dumps(lr_trial(lr, T)), i, 0, i)
+    e.on_complete(lambda node, end, subs: e.cancel(0, 1) if [0, 0] in [list(s) for s in subs] else None)
+    e.run()
+    st = json.loads(e.stats())
+    assert st["releases"] == 0 and st["stage_steps"] == 200 and [s for s, _, _ in e.history(0, 2)] == [20, 200]
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_checkpoint_gc_frees_instead_of_spilling(seed):
+    rng = random.Random(500 + seed)
+    trials = random_trials(rng)
+    runs = {}
+    for gc in (False, True):
+        e, _, st = run(trials, slots_per_gpu=2, ckpts_per_gpu=3, ckpt_gc=gc)
+        runs[gc] = (st, {t: e.history(*t) for t in e.trials()})
+    (s0, h0), (s1, h1) = runs[False], runs[True]
+    assert h0 == h1                       # GC never changes results
+    assert s1["spills"] <= s0["spills"]   # dead entries are freed, not spilled
+    assert s0["gc_frees"] == 0
+    if s0["spills"]:
+        assert s1["gc_frees"] > 0 or s1["spills"] == s0["spills"]
+
+
+def test_collect_checkpoints_keeps_what_live_trials_need():
+    e = engine(KEY_LR, slots_per_gpu=2, ckpts_per_gpu=64, eval_intervals=[40])
+    for i, (lr, T) in enumerate([("0.1", 100), ("0.1", 200), ("0.01", 150)]):
+        e.submit(json.dumps(lr_trial(lr, T)), i, 0, i)
+    e.run()
+    saves = json.loads(e.stats())["saves"]
+    freed = e.collect_checkpoints()
+    # the eval-mark checkpoints (40, 80, 120, 160) go; each live trial's end checkpoint stays
+    assert saves == 10 and freed == 7
+    # an EXTEND of trial 1 resumes from its kept end checkpoint: no retraining of [0, 200)
+    e.submit(json.dumps(lr_trial("0.1", 260)), 10, 0, 1)
+    before = json.loads(e.stats())["stage_steps"]
+    e.run()
+    assert json.loads(e.stats())["stage_steps"] - before == 60
+
+
+def test_set_runtime_fed_from_profile_table():
+    key = {"model": "mlp", "dataset": "synthetic", "hp_set": ["batch_size", "lr"]}
+    cfg = lambda lr, bs: {"total_steps": 100, "hps": {
+        "lr": [{"fn": {"family": "constant", "value": lr}, "local_start": 0, "duration": 100}],
+        "batch_size": [{"fn": {"family": "constant", "value": bs}, "local_start": 0, "duration": 100}]}}
+    e = engine(key, slots_per_gpu=2, step_cost_us={"128": 51.5, "256": 97.25})
+    e.submit(json.dumps(cfg("0.1", 128)), 0, 0, 0)
+    e.submit(json.dumps(cfg("0.1", 256)), 1, 0, 1)
+    e.run()
+    plan = json.loads(e.plan_json())
+    rt = sorted(n["runtime_sec_per_step"] for n in plan["nodes"])
+    assert rt == pytest.approx([51.5e-6, 97.25e-6], rel=1e-12)
+
+
+def test_trace_determinism_and_accounting():
+    rng = random.Random(77)
+    trials = random_trials(rng)
+    tr = []
+    for _ in range(2):
+        e, shape, st = run(trials, slots_per_gpu=3, eval_intervals=[40])
+        tr.append(e.trace())
+    assert tr[0] == tr[1]  # acceptance 10: byte-identical traces
+    ev = tr[0]
+    kinds = {k for _, _, k, *_ in ev}
+    assert kinds <= {"LOAD", "TRAIN", "SAVE", "EVAL", "IDLE"}
+    # TRAIN durations sum to the executed stage-steps; per worker they never overlap
+    assert sum(end - start for _, _, k, _, start, end, _ in ev if k == "TRAIN") == st["stage_steps"]
+    per = {}
+    for t, w, k, _, start, end, _ in ev:
+        if k == "TRAIN":
+            per.setdefault(w, []).append((t, t + end - start))
+    for spans in per.values():
+        spans.sort()
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+    # every trial is reported exactly once, at its end step, by an EVAL event
+    seen = {}
+    for _, _, k, _, start, end, d in ev:
+        if k == "EVAL" and "trials=" in d:
+            for s in d.split("trials=")[1].split(","):
+                seen.setdefault(s, []).append(end)
+    assert sorted(seen) == sorted(f"0:{i}" for i in range(len(trials)))
+    assert all(seen[f"0:{i}"] == [c["total_steps"]] for i, c in enumerate(trials))
