@@ -152,6 +152,7 @@ struct ConvArgs {
     int x_from_slot;     // 1: first row = slot data offset (training); 0: x_row0 (eval chunk)
     int x_row0;
     int fixed_bs;        // > 0: batch size override (eval chunks)
+    int fuse_update;     // tensor-core lockstep: the weight-gradient reductions apply K5 in place
     float* slab;
     long long slab_stride;
     float* act;
@@ -484,7 +485,7 @@ struct Fwd {
     // the producers also record the ReLU mask of the layer input (conv2: a1, conv3: a2) as a bitmap
     // for the input gradient of this layer: the taps (kh, kw) in {1, 2}^2 of a stride-2 conv visit
     // every input pixel exactly once, and a producer thread holds 32 consecutive channels of it
-    static constexpr bool kInMaskBits = (L >= 2), kMaskFromBits = false;
+    static constexpr bool kInMaskBits = (L >= 2), kMaskFromBits = false, kSgd = false;
     uint32_t* in_bits;
     const CUtensorMap* tmap;
     const float* in;
@@ -589,7 +590,7 @@ struct Dgrad {
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
     static constexpr bool A_TMA = true;  // A tile = one shifted TMA box of dy per chunk
-    static constexpr bool kInMaskBits = false, kMaskFromBits = true;
+    static constexpr bool kInMaskBits = false, kMaskFromBits = true, kSgd = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
     const CUtensorMap* tmap;
@@ -677,7 +678,7 @@ struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = (L >= 2);
-    static constexpr bool kInMaskBits = false, kMaskFromBits = false;
+    static constexpr bool kInMaskBits = false, kMaskFromBits = false, kSgd = false;
     // TMA: a tile's 128 rows are 128 / Ci taps x Ci channels; one box per tap = 32 output pixels
     // (the chunk's reduction indices) x Ci channels, stored [tap][pixel][ci]
     static constexpr int kBoxes = 128 / G::Ci, kTmaCi = G::Ci;
@@ -1039,44 +1040,62 @@ __global__ void __launch_bounds__(256, 2) conv1_wgrad_lane(ConvArgs p) {
     }
 }
 
-// Sum the per-sample partials in sample order into the gradient slab.  grid (7, groups), block 128.
+// Sum the per-sample partials in sample order into the gradient slab, or (fuse_update) apply K5
+// to the parameter in place.  grid (7, groups), block 128.
 __global__ void __launch_bounds__(128) conv1_wgrad_reduce(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* part = v.act + p.al.w1p;
     float* g = p.grad + p.grad_stride * v.slot;
+    float* w = p.slab + p.slab_stride * v.slot;
+    float* m = w + p.slab_stride / 2;
+    const SgdRow h = sgd_row(p.hp, p.hp_cap, p.st, v.slot);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kL1Outs; i += gridDim.x * blockDim.x) {
         float s_ = 0.0f;
 #pragma unroll 8
         for (int n = 0; n < v.bs; ++n) s_ = __fadd_rn(s_, __ldg(part + (long long)n * kL1Outs + i));
         const int co = i / 28, j = i % 28;
-        if (j < 27)
-            g[Geo<1>::OffW + (co * 9 + j / 3) * 4 + j % 3] = s_;
+        const long long at = j < 27 ? Geo<1>::OffW + (co * 9 + j / 3) * 4 + j % 3 : Geo<1>::OffB + co;
+        if (p.fuse_update)
+            sgd_apply(w, m, at, s_, h);
         else
-            g[Geo<1>::OffB + co] = s_;
+            g[at] = s_;
     }
-    // the padded input channel's weights stay exactly zero
-    if (blockIdx.x == 0)
+    // the padded input channel's weights stay exactly zero (gradient 0; w = m = 0 untouched)
+    if (blockIdx.x == 0 && !p.fuse_update)
         for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) g[Geo<1>::OffW + i * 4 + 3] = 0.0f;
 }
 
 // Weight-gradient reduction: grad[W][co][k] = sum_{s asc} part[s][co][k] (k < 9 Ci), grad[b][co]
-// from the all-ones row.  grid (Co, groups), block 128.
+// from the all-ones row; with fuse_update the sum is the gradient K5 applies in place (K3+K5:
+// no gradient slab round trip).  grid (Co [+ kFcBlocks for L = 3 fused], groups), block 128.
+// The fused L = 3 launch also updates the FC layer (W4 | b4, gradients from head_grad_kernel):
+// it runs on the weight-gradient branch after head_dg_kernel, the last reader of W4.
+constexpr int kFcParams = kNCP * kFeat + kNCP, kFcBlocks = (kFcParams + 127) / 128;
 template <int L>
 __global__ void __launch_bounds__(128) wgrad_reduce_kernel(ConvArgs p) {
     using G = Geo<L>;
     using P = Part<L>;
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
+    float* w = p.slab + p.slab_stride * v.slot;
+    float* m = w + p.slab_stride / 2;
+    float* g = p.grad + p.grad_stride * v.slot;
+    const SgdRow h = sgd_row(p.hp, p.hp_cap, p.st, v.slot);
+    if ((int)blockIdx.x >= G::Co) {  // L = 3, fused: the FC parameters
+        const int i = (blockIdx.x - G::Co) * 128 + threadIdx.x;
+        if (i < kFcParams) sgd_apply(w, m, kOffW4 + i, __ldcs(g + kOffW4 + i), h);
+        return;
+    }
     const int co = blockIdx.x;
     const int nsplit = (v.bs * G::OH * G::OH + kSplitRows - 1) / kSplitRows;
     const float* part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3) + (long long)co * P::Ld;
-    float* g = p.grad + p.grad_stride * v.slot;
     for (int k = threadIdx.x; k < P::Rows; k += blockDim.x) {
         float s = 0.0f;
         for (int i = 0; i < nsplit; ++i) s = __fadd_rn(s, part[(long long)i * G::Co * P::Ld + k]);
-        if (k < 9 * G::Ci)
-            g[G::OffW + (long long)co * 9 * G::Ci + k] = s;
+        const long long at = k < 9 * G::Ci ? G::OffW + (long long)co * 9 * G::Ci + k : G::OffB + co;
+        if (p.fuse_update)
+            sgd_apply(w, m, at, s, h);
         else
-            g[G::OffB + co] = s;
+            g[at] = s;
     }
 }
 

@@ -596,6 +596,14 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 const int m = mt0 + row;
                 if (m < M)
                     for (int col = 32 * ch; col < N; col += 32 * (Plan::EpiWarps / 4)) prefetch_l2(op.mask_at(m, col));
+            } else if constexpr (Op::kSgd) {
+                // SGD epilogue: warm L2 with the tile's parameters and momenta while the MMAs run
+                const int m = mt0 + row;
+                if (m < M)
+                    for (int col = 32 * ch; col < N; col += 32 * (Plan::EpiWarps / 4)) {
+                        prefetch_l2(op.w_at(m, col));
+                        prefetch_l2(op.w_at(m, col) + op.m_off);
+                    }
             }
             // sum the tile's segments (round-to-nearest fp32 adds, fixed order): in registers when
             // a warp drains at most 64 columns, then once into sacc; otherwise in sacc directly
@@ -700,6 +708,39 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 float4 bfix = make_float4(0.f, 0.f, 0.f, 0.f);
                 if constexpr (Op::EPI != ctc::kEpiStore)
                     if (fixed_c4) bfix = op.bias4(4 * (et % q4));
+                if constexpr (Op::kSgd) {
+                    // K3+K5: the tile is the weight gradient; apply the update to w | m in place,
+                    // U quads per thread with their loads issued before any use
+                    constexpr int U = 4;
+                    if ((op.ldc & 3) == 0 && (N & 3) == 0) {
+                        for (int e0 = et; e0 < kBM * q4; e0 += U * Plan::EpiThreads) {
+                            float4 wv[U], mv[U];
+                            float* wp[U];
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const int e = e0 + u * Plan::EpiThreads, r = e / q4, c4 = e % q4, m = mt0 + r;
+                                wp[u] = (e < kBM * q4 && m < M) ? op.w_at(m, 4 * c4) : nullptr;
+                                if (wp[u]) {
+                                    wv[u] = *reinterpret_cast<const float4*>(wp[u]);
+                                    mv[u] = *reinterpret_cast<const float4*>(wp[u] + op.m_off);
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                if (!wp[u]) continue;
+                                const int e = e0 + u * Plan::EpiThreads, r = e / q4, c4 = e % q4;
+                                op.sgd4(wv[u], mv[u], *s4(r, c4));
+                                *reinterpret_cast<float4*>(wp[u]) = wv[u];
+                                *reinterpret_cast<float4*>(wp[u] + op.m_off) = mv[u];
+                            }
+                        }
+                    } else {
+                        for (int e = et; e < kBM * q4; e += Plan::EpiThreads) {
+                            const int r = e / q4, c4 = e % q4, m = mt0 + r;
+                            if (m < M && 4 * c4 < N) op.store4(m, 4 * c4, *s4(r, c4));
+                        }
+                    }
+                } else
                 for (int e = et; e < kBM * q4; e += Plan::EpiThreads) {
                     const int r = e / q4, c4 = e % q4, m = mt0 + r;
                     if (m >= M) continue;

@@ -5,7 +5,9 @@
 // AM / BMODE: 0 -> K-contiguous rows (X[m*ld + k]), 1 -> MN-contiguous (X[k*ld + m]).  M or K may
 // be the slot's batch size; one N tile of up to 128 columns per blockIdx.x.  A_EXACT / B_EXACT
 // mark an operand that is exact in tf32 (the synthetic data, k/128) so its lo MMA is skipped.
-// Epilogues: bias(+ReLU), plain, ReLU mask (dH = (H > 0) ? . : 0), transposed store.
+// Epilogues: bias(+ReLU), plain, ReLU mask (dH = (H > 0) ? . : 0), transposed store; SGD = a
+// plain-store weight gradient whose tile is applied to the slot's w | m in place (K3+K5 fusion,
+// the sgd_update_kernel rule element by element).
 #pragma once
 
 #include "conv_ws.cuh"
@@ -19,13 +21,13 @@ using cnn::ctc::kEpiMask;
 using cnn::ctc::kEpiPartT;
 using cnn::ctc::kEpiStore;
 
-template <int AM_, int BM_, int EPI_, bool AX, bool BX>
+template <int AM_, int BM_, int EPI_, bool AX, bool BX, bool SGD = false>
 struct DenseOp {
     using Args = GemmArgs;
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
     static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false;
     static constexpr int kBoxes = 1, kTmaCi = 1;
-    static constexpr bool kInMaskBits = false, kMaskFromBits = false;
+    static constexpr bool kInMaskBits = false, kMaskFromBits = false, kSgd = SGD;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;
     const float* A;
     const float* B;
@@ -34,6 +36,8 @@ struct DenseOp {
     const float* mask;
     int lda, ldb, ldc, ldmask;
     int M, N, K, kbeg, m0, split, n0;
+    long long m_off;
+    SgdRow h;
 
     __device__ void setup(const GemmArgs& p, int z, int x) {
         const int slot = p.slots[z];
@@ -55,6 +59,8 @@ struct DenseOp {
         bias = (EPI == kEpiBias || EPI == kEpiBiasRelu) ? p.bias + p.bias_stride * slot : nullptr;
         mask = EPI == kEpiMask ? p.mask + p.mask_stride * slot : nullptr;
         ldmask = p.ldmask;
+        m_off = p.m_off;
+        if (SGD) h = sgd_row(p.hp, p.hp_cap, p.st, slot);
     }
 
     // ---- A, K-contiguous: row pointer once per tile, k per chunk
@@ -97,6 +103,25 @@ struct DenseOp {
     }
     __device__ __forceinline__ void store4(int m, int col, float4 x) const {
         float* c = C + (long long)m * ldc + n0 + col;
+        if constexpr (SGD) {
+            static_assert(EPI == kEpiStore, "the SGD epilogue consumes a plain gradient tile");
+            const float v[4] = {x.x, x.y, x.z, x.w};
+            if ((ldc & 3) == 0 && col + 4 <= N) {
+                float4 wv = *reinterpret_cast<float4*>(c), mv = *reinterpret_cast<float4*>(c + m_off);
+                float* wp = &wv.x;
+                float* mp = &mv.x;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    mp[j] = __fmaf_rn(h.mu, mp[j], __fmaf_rn(h.wd, wp[j], v[j]));
+                    wp[j] = __fmaf_rn(h.nlr, mp[j], wp[j]);
+                }
+                *reinterpret_cast<float4*>(c) = wv;
+                *reinterpret_cast<float4*>(c + m_off) = mv;
+            } else {
+                for (int j = 0; j < 4 && col + j < N; ++j) sgd_apply(c, c + m_off, j, v[j], h);
+            }
+            return;
+        }
         if ((ldc & 3) == 0 && n0 + col + 4 <= n0 + N) {
             *reinterpret_cast<float4*>(c) = x;
         } else {
@@ -105,6 +130,18 @@ struct DenseOp {
         }
     }
     __device__ __forceinline__ const void* mask_at(int m, int col) const { return mask + (long long)m * ldmask + n0 + col; }
+    // SGD epilogue: the parameter at (m, col) of the tile (w; its momentum at + m_off)
+    __device__ __forceinline__ float* w_at(int m, int col) const { return C + (long long)m * ldc + n0 + col; }
+    __device__ __forceinline__ void sgd4(float4& w, float4& m, float4 g) const {
+        m.x = __fmaf_rn(h.mu, m.x, __fmaf_rn(h.wd, w.x, g.x));
+        m.y = __fmaf_rn(h.mu, m.y, __fmaf_rn(h.wd, w.y, g.y));
+        m.z = __fmaf_rn(h.mu, m.z, __fmaf_rn(h.wd, w.z, g.z));
+        m.w = __fmaf_rn(h.mu, m.w, __fmaf_rn(h.wd, w.w, g.w));
+        w.x = __fmaf_rn(h.nlr, m.x, w.x);
+        w.y = __fmaf_rn(h.nlr, m.y, w.y);
+        w.z = __fmaf_rn(h.nlr, m.z, w.z);
+        w.w = __fmaf_rn(h.nlr, m.w, w.w);
+    }
     __device__ __forceinline__ long long mask_off(int m, int col) const {
         return (long long)m * ldmask + n0 + col;
     }

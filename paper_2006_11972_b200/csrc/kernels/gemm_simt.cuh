@@ -37,6 +37,7 @@ struct GemmArgs {
     const float* hp;
     int hp_cap;
     int n_train_mask;
+    long long m_off;  // sgd epilogue (tensor-core weight gradient): C points at w, momentum at C + m_off
 };
 
 enum Epi { kEpiStore = 0, kEpiBiasRelu = 1, kEpiBias = 2, kEpiMask = 3 };

@@ -193,6 +193,59 @@ __global__ void __launch_bounds__(256) sgd_update_kernel(StepCtx c, float* slab,
     }
 }
 
+// K5 fused into a gradient producer (K3+K5): the same rule as sgd_update_kernel, applied by the
+// kernel that computes the parameter's final gradient, so the gradient never round-trips through
+// HBM (8 B/param/step).  Bitwise identical to storing g and running sgd_update_kernel.
+struct SgdRow {
+    float nlr, mu, wd;
+};
+__device__ __forceinline__ SgdRow sgd_row(const float* hp, int hp_cap, const SlotState* st, int slot) {
+    const float* r = hp + ((long long)slot * hp_cap + st[slot].step) * 4;
+    return SgdRow{-r[0], r[1], r[2]};
+}
+__device__ __forceinline__ void sgd_apply(float* w, float* m, long long i, float g, const SgdRow& h) {
+    const float mv = __fmaf_rn(h.mu, m[i], __fmaf_rn(h.wd, w[i], g));
+    m[i] = mv;
+    w[i] = __fmaf_rn(h.nlr, mv, w[i]);
+}
+
+// Tensor-core MLP lockstep, after the last weight-gradient GEMM (layer 1, whose epilogue updates
+// W1 in place): blocks [0, nb): the layer-1 bias gradient (colsum_fast order) with the update
+// fused; blocks [nb, ...): the update of the parameter range [lo, hi) (W2, b2, W3, b3) from the
+// gradient slab -- every reader of those weights (the input-gradient GEMMs) has finished.
+__global__ void __launch_bounds__(256) colsum_sgd_kernel(StepCtx c, const float* act, long long act_stride,
+                                                         long long dy_off, int ld, int N, float* slab,
+                                                         long long slab_stride, const float* grad,
+                                                         long long grad_stride, long long db_off, int nb,
+                                                         long long lo, long long hi) {
+    const int slot = c.slots[blockIdx.y];
+    const SgdRow h = sgd_row(c.hp, c.hp_cap, c.st, slot);
+    float* w = slab + slab_stride * slot;
+    float* m = w + slab_stride / 2;
+    if ((int)blockIdx.x < nb) {
+        const int B = (int)hp_row(c, slot)[3];
+        const int col = threadIdx.x & 31, lane_r = threadIdx.x >> 5;
+        const int n = blockIdx.x * 32 + col;
+        __shared__ float part[8][33];
+        const float* dY = act + act_stride * slot + dy_off;
+        float s = 0.0f;
+        if (n < N)
+            for (int r = lane_r; r < B; r += 8) s = __fadd_rn(s, dY[(long long)r * ld + n]);
+        part[lane_r][col] = s;
+        __syncthreads();
+        if (lane_r == 0 && n < N) {
+            float t = part[0][col];
+            for (int i = 1; i < 8; ++i) t = __fadd_rn(t, part[i][col]);
+            sgd_apply(w, m, db_off + n, t, h);
+        }
+        return;
+    }
+    const float* g = grad + grad_stride * slot;
+    for (long long i = lo + ((long long)blockIdx.x - nb) * blockDim.x + threadIdx.x; i < hi;
+         i += (long long)(gridDim.x - nb) * blockDim.x)
+        sgd_apply(w, m, i, __ldcs(g + i), h);
+}
+
 // Advance each active slot by one step: step += 1, offset += bs.
 __global__ void advance_kernel(StepCtx c, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -162,6 +162,11 @@ void tc_launch(smx_ctx* c, const GemmArgs& a, int groups, int m_max) {
         if (a.a.from_data && c->data_tf32_exact) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, true, false>>(c, a, groups, m_max);
     }
     if constexpr (AM == 1 && BMODE == 1 && EPI == tc::kTcStore) {
+        if (a.m_off) {  // layer-1 weight gradient with the K5 update fused into its epilogue
+            if (a.b.from_data && c->data_tf32_exact)
+                return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, true, true>>(c, a, groups, m_max);
+            return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, false, true>>(c, a, groups, m_max);
+        }
         if (a.b.from_data && c->data_tf32_exact) return dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, true>>(c, a, groups, m_max);
     }
     dense_ws_launch<dws::DenseOp<AM, BMODE, wepi, false, false>>(c, a, groups, m_max);
@@ -254,6 +259,7 @@ cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
     a.labels = c->ytrain;
     a.loss_hist = c->loss;
     a.tmaps = c->tmaps;
+    a.fuse_update = c->d.gemm_mode == SMX_GEMM_TC ? 1 : 0;
     return a;
 }
 
@@ -316,7 +322,8 @@ void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     if (c->d.gemm_mode == SMX_GEMM_TC) {
         const int splits = (mb * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
         conv_tc<cnn::ctc::Wgrad<L>>(c, a, splits, cnn::Part<L>::Rows, n);
-        cnn::wgrad_reduce_kernel<L><<<dim3(G::Co, n), 128, 0, c->cur>>>(a);
+        const int fc = (L == 3 && a.fuse_update) ? cnn::kFcBlocks : 0;  // + the FC layer's update
+        cnn::wgrad_reduce_kernel<L><<<dim3(G::Co + fc, n), 128, 0, c->cur>>>(a);
         launch_check(c, "wgrad_reduce");
         return;
     }
@@ -387,14 +394,18 @@ void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
     ck(cudaEventRecord(c->fj[3], c->side), "join record");
     ck(cudaStreamWaitEvent(c->stream, c->fj[3], 0), "join wait");
     c->cur = c->stream;
-    if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-    {
+    if (c->d.gemm_mode == SMX_GEMM_TC && c->timing) {  // fused: no separate update interval
+        cudaEventRecord(c->ev[2], c->stream);
+        cudaEventRecord(c->ev[3], c->stream);
+    }
+    if (c->d.gemm_mode != SMX_GEMM_TC) {  // tensor-core mode: K5 fused into the reductions
+        if (c->timing) cudaEventRecord(c->ev[2], c->stream);
         const long long n4 = c->palloc / 4;
         const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
         sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, c->slab, c->slab_stride(), c->grad, c->palloc, n4);
         launch_check(c, "sgd_update");
+        if (c->timing) cudaEventRecord(c->ev[3], c->stream);
     }
-    if (c->timing) cudaEventRecord(c->ev[3], c->stream);
     advance_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(sc, n);
     launch_check(c, "advance");
 }
@@ -531,28 +542,44 @@ void enqueue_lockstep(smx_ctx* c, const int* d_slots, int n) {
         // ---- layer 1 grads
         fork(2);
         c->cur = c->side;
+        const bool fused = c->d.gemm_mode == SMX_GEMM_TC;
         {
             GemmArgs g = base_args(c, d_slots);
             g.a = Opnd{A + kActDH1, AS, kH, 0};
             g.b = Opnd{c->xtrain, 0, kD0, 1};
-            g.c = G + kOffW1; g.c_stride = kPAlloc; g.ldc = kD0;
             g.M = kH; g.N = kD0; g.K = mb; g.k_is_bs = 1;
+            if (fused) {  // K3+K5: the epilogue updates W1 in place (tensor-core mode)
+                g.c = W + kOffW1; g.c_stride = SW; g.ldc = kD0; g.m_off = kPAlloc;
+            } else {
+                g.c = G + kOffW1; g.c_stride = kPAlloc; g.ldc = kD0;
+            }
             gemm<1, 1, kEpiStore>(c, g, n, kH);
         }
-        colsum(c, sc, n, kActDH1, kH, kH, kOffB1);
+        if (c->timing) cudaEventRecord(c->ev[2], c->cur);
+        if (fused) {
+            // b1 with its update fused, then W2 b2 W3 b3 from the gradient slab: the input-gradient
+            // GEMMs (their only readers after the forward) finished before fork(2)
+            const int nb = (kH + 31) / 32;
+            colsum_sgd_kernel<<<dim3(nb + 64, n), 256, 0, c->side>>>(sc, c->act, kActStride, kActDH1, kH, kH, W, SW, G,
+                                                                     kPAlloc, kOffB1, nb, kOffW2, kPEnd);
+            launch_check(c, "colsum_sgd");
+        } else {
+            colsum(c, sc, n, kActDH1, kH, kH, kOffB1);
+        }
+        if (c->timing) cudaEventRecord(c->ev[3], c->cur);
         ck(cudaEventRecord(c->fj[3], c->side), "join record");
         ck(cudaStreamWaitEvent(c->stream, c->fj[3], 0), "join wait");
         c->cur = c->stream;
     }
-    // ---- K5 update + advance
-    if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-    {
+    // ---- K5 update (exact mode; tensor-core mode fused it above) + advance
+    if (c->d.gemm_mode != SMX_GEMM_TC) {
+        if (c->timing) cudaEventRecord(c->ev[2], c->stream);
         const long long n4 = kPAlloc / 4;
         const int bx = (int)((n4 + 256 * 4 - 1) / (256 * 4));
         sgd_update_kernel<<<dim3(bx, n), 256, 0, c->stream>>>(sc, W, SW, G, kPAlloc, n4);
         launch_check(c, "sgd_update");
+        if (c->timing) cudaEventRecord(c->ev[3], c->stream);
     }
-    if (c->timing) cudaEventRecord(c->ev[3], c->stream);
     advance_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(sc, n);
     launch_check(c, "advance");
 }
@@ -694,6 +721,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         c->device = device;
         c->S = n_slots;
         c->C = n_ckpts;
+        c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 13 : 14;  // MLP (TC: K5 fused)
         if (d.model == SMX_MODEL_CNN) {
             if (d.n_val % d.max_batch) fail(SMX_ECONFIG, "CNN: n_val must be a multiple of max_batch");
             c->cnn = true;
@@ -701,7 +729,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             c->al = cnn::act_layout(d.max_batch);
             c->act_stride = c->al.stride;
             c->d_in = cnn::kSample;
-            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 19 : 13;
+            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 18 : 13;
         }
         try {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
