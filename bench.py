@@ -457,6 +457,40 @@ def main():
         roofline["kernel"] = "conv_ws_kernel<DenseOp<0,0,BiasRelu,exact A>> (MLP layer-1 forward, 64 groups x 128x256x784)"
     roofline["traffic"] = TRAFFIC.get(roofline["kernel"].split(" ")[0])
 
+    # ---- K7: checkpoint fork to another GPU (smx_ckpt_peer_copy, NVLink P2P); on a 1-GPU box the
+    # same call between two contexts of the one device (a device-local copy), labelled as such
+    k7 = None
+    if rank == 0 and world == 1:
+        ndev = torch.cuda.device_count()
+        src_dev, dst_dev = local, (local + 1) % ndev if ndev > 1 else local
+        mk = dict(max_steps=8, max_batch=8, n_train=4096, n_val=256, gemm_mode=gemm_mode,
+                  model=ex.MODEL_CNN if cnn else ex.MODEL_MLP)
+        n7 = 32
+        src = ex.Executor(n_slots=1, n_ckpts=n7, device=src_dev, **mk)
+        dst = ex.Executor(n_slots=1, n_ckpts=n7, device=dst_dev, **mk)
+        src.slot_init(0)
+        for i in range(n7):
+            src.slot_save(0, i)
+        for i in range(n7):
+            dst.ckpt_peer_copy(i, src, i)
+        dst.set_timing(True)
+        dst.reset_stats()
+        for _ in range(3):
+            for i in range(n7):
+                dst.ckpt_peer_copy(i, src, i)
+        kst = dst.stats()
+        ms7 = kst["fork_ms"] / kst["fork_launches"]
+        b7 = 8 * src.p_alloc + 16  # w | m + step / offset, one direction
+        link = src_dev != dst_dev
+        a7 = b7 / (ms7 * 1e-3) / 1e9
+        k7 = {"bound": "nvlink" if link else "hbm (same device: no peer on this box)", "achieved": a7,
+              "peak": 900.0 if link else pk["hbm_gbs"], "unit": "GB/s",
+              "frac": a7 / (900.0 if link else pk["hbm_gbs"]), "bytes_per_copy": b7, "ms_per_copy": ms7,
+              "devices": [src_dev, dst_dev],
+              "note": "one checkpoint per call (the engine's cross-GPU LOAD); latency-bound at this size"}
+        src.close()
+        dst.close()
+
     cpu = None
     if rank == 0 and not args.no_cpu and not tuned and world == 1:
         cpu = CpuReference(args.workload, max_batch).sample(20.0)
@@ -477,7 +511,7 @@ def main():
                     "h2d_bytes_per_step": st_e["h2d_bytes"], "d2h_bytes_per_step": st_e["d2h_bytes"]},
             "gpu_launches": st["kernel_launches"] * args.steps,
             "roofline": roofline,
-            "kernels": kernels,
+            "kernels": {**kernels, **({"K7_peer_fork": k7} if k7 else {})},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "engine_stats": st,

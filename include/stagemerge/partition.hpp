@@ -24,4 +24,13 @@ void assign_roots(const SearchPlan& plan, int world, std::map<NodeId, int>& owne
 /// Root of the subtree containing `node`.
 NodeId root_of(const SearchPlan& plan, NodeId node);
 
+/// In-process placement of every plan node on one of `devices` GPUs: LPT over
+/// placement units by step extent.  Units start as root subtrees; while the heaviest unit
+/// exceeds total / devices it is split at its first branch point -- every child subtree but the
+/// heaviest becomes its own unit -- so one dominant root no longer serialises on one GPU.  A
+/// split-off subtree's first stage LOADs its branch checkpoint from the parent's GPU with one
+/// peer copy (K7).  Deterministic (plan only); ties: heavier first, then smaller node id, then
+/// the lowest device.
+std::map<NodeId, int> place_nodes(const SearchPlan& plan, int devices);
+
 }  // namespace stagemerge

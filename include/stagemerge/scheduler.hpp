@@ -3,6 +3,7 @@
 // from the SPEC.
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "stagemerge/stage_tree.hpp"
@@ -22,5 +23,16 @@ struct Assignment {
 /// lowest worker id first, until workers or unscheduled root paths run out.  Holds no state.
 std::vector<Assignment> schedule(const SearchPlan& plan, const TreeBuildContext& ctx, const std::vector<int>& idle_workers,
                                  const StepTimeEstimator& step_us, int first_assignment_id = 0);
+
+/// Multi-GPU form ("fill the least-loaded GPU's free slots" behind the same
+/// critical-path rule): idle workers grouped per device; a critical path goes to the lowest-id
+/// idle worker of the device its first stage's node is placed on, cut before its first stage on
+/// another device (that remainder resumes from the cut's checkpoint -- saved at the stage end --
+/// in a later round, on its own device, via a peer copy).  A path whose device has no idle
+/// worker is passed over this round.  With one device this is exactly schedule().
+std::vector<Assignment> schedule_placed(const SearchPlan& plan, const TreeBuildContext& ctx,
+                                        const std::vector<std::vector<int>>& idle_by_device,
+                                        const std::function<int(NodeId)>& device_of, const StepTimeEstimator& step_us,
+                                        int first_assignment_id = 0);
 
 }  // namespace stagemerge

@@ -76,13 +76,14 @@ Engine::Engine(CompatKey key, EngineOptions opts) : key_(std::move(key)), opts_(
         for (int e = opts_.ckpts_per_gpu - 1; e >= 0; --e) g->free_entries.push_back(e);
         gpus_.push_back(std::move(g));
     }
-    // worker w -> GPU w % G, slot w / G: "lowest idle worker first" spreads paths over GPUs
+    // worker w -> GPU w / S, slot w % S; with several GPUs, paths go to the GPU their nodes are
+    // placed on (place_nodes, schedule_placed)
     const int G = static_cast<int>(gpus_.size());
     for (int w = 0; w < G * opts_.slots_per_gpu; ++w) {
         auto wk = std::make_unique<Worker>();
         wk->id = w;
-        wk->gpu = w % G;
-        wk->slot = w / G;
+        wk->gpu = w / opts_.slots_per_gpu;
+        wk->slot = w % opts_.slots_per_gpu;
         workers_.push_back(std::move(wk));
     }
 }
@@ -467,7 +468,16 @@ void Engine::dispatch() {
     TreeBuildContext ctx;
     ctx.running = blocked_nodes();
     ctx.eval_intervals = opts_.eval_intervals;
-    const auto as = schedule(*plan_, ctx, idle, [this](NodeId n) { return est_us(n); }, next_assignment_);
+    const auto est = [this](NodeId n) { return est_us(n); };
+    std::vector<Assignment> as;
+    if (gpus_.size() == 1) {
+        as = schedule(*plan_, ctx, idle, est, next_assignment_);
+    } else {
+        const std::map<NodeId, int> place = place_nodes(*plan_, static_cast<int>(gpus_.size()));
+        std::vector<std::vector<int>> by_dev(gpus_.size());
+        for (int w : idle) by_dev[static_cast<std::size_t>(workers_[static_cast<std::size_t>(w)]->gpu)].push_back(w);
+        as = schedule_placed(*plan_, ctx, by_dev, [&place](NodeId n) { return place.at(n); }, est, next_assignment_);
+    }
     next_assignment_ += static_cast<int>(as.size());
     for (const Assignment& a : as) start(a);
 }

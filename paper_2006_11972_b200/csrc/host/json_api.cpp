@@ -241,6 +241,11 @@ json run(const json& cmd) {
             for (const auto& [r, w] : root_work(plan)) work[std::to_string(r)] = w;
             out["partition"] = {{"owner", own}, {"work", work}};
         }
+        if (cmd.contains("placement")) {
+            json pl = json::object();
+            for (const auto& [n, d] : place_nodes(plan, cmd.at("placement").get<int>())) pl[std::to_string(n)] = d;
+            out["placement"] = pl;
+        }
     } else {
         throw ConfigError("unknown op " + op);
     }

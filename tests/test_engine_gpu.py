@@ -122,3 +122,34 @@ def test_partitioned_ranks_cover_all_roots():
     assert owned[0].isdisjoint(owned[1]) and owned[0] | owned[1] == {0, 3}
     ref = run(spec, slots_per_gpu=4).histories()
     assert hist == ref
+
+
+def dominant_root_spec(n=16, total=120):
+    """16 trials on one root (lr 0.1 for 40 steps) branching at 40 and 80: one subtree holds all
+    the work, so the multi-GPU placement splits it and the split-off subtrees LOAD by peer copy."""
+    trials = []
+    for i in range(n):
+        trials.append({"hps": {"lr": {"family": "step", "values": ["0.1", ["0.05", "0.02", "0.01", "0.005"][i % 4],
+                                                                  ["0.003", "0.002", "0.001", "0.0005"][i // 4]],
+                                      "milestones": [40, 80]}}})
+    return json.dumps({"schema": 1, "name": "dominant", "model": "mlp", "max_steps": total, "eval_interval": 40,
+                       "trials": trials})
+
+
+@pytest.mark.parametrize("spec_name", ["c1_fig1", "dominant"])
+def test_two_contexts_equal_one_device(spec_name):
+    """Engine(devices=[0, 0]): two executor contexts on the one B200, paths placed by subtree
+    (place_nodes / schedule_placed); split-off subtrees LOAD through smx_ckpt_peer_copy (K7).
+    Every trial's history is bitwise the single-context run's and no step is re-executed."""
+    spec = host.study_spec("c1_fig1") if spec_name == "c1_fig1" else dominant_root_spec()
+    one = run(spec, slots_per_gpu=4)
+    two = run(spec, slots_per_gpu=4, devices=[0, 0])
+    assert two.histories() == one.histories()
+    s1, s2 = one.stats(), two.stats()
+    assert s1["stage_steps"] == s2["stage_steps"] and s1["trial_steps"] == s2["trial_steps"]
+    if spec_name == "dominant":
+        assert s2["peer_copies"] > 0
+    # tensor-core mode too (grouping invariance across contexts)
+    one_tc = run(spec, slots_per_gpu=4, gemm_mode=1)
+    two_tc = run(spec, slots_per_gpu=4, gemm_mode=1, devices=[0, 0])
+    assert two_tc.histories() == one_tc.histories()

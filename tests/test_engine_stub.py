@@ -252,3 +252,65 @@ def test_trace_determinism_and_accounting():
                 seen.setdefault(s, []).append(end)
     assert sorted(seen) == sorted(f"0:{i}" for i in range(len(trials)))
     assert all(seen[f"0:{i}"] == [c["total_steps"]] for i, c in enumerate(trials))
+
+
+# ---------------------------------------------------------------- in-process multi-GPU (§8e)
+
+def dominant_root_trials(n=16, total=300, momentum=True):
+    """One root (lr 0.1 for the first 100 steps) carries every trial; they branch at 100 / 200."""
+    out = []
+    for i in range(n):
+        segs = [{"fn": {"family": "constant", "value": "0.1"}, "local_start": 0, "duration": 100},
+                {"fn": {"family": "constant", "value": ["0.05", "0.02", "0.01", "0.005"][i % 4]}, "local_start": 0,
+                 "duration": 100},
+                {"fn": {"family": "constant", "value": ["0.003", "0.002", "0.001", "0.0005"][i // 4]},
+                 "local_start": 0, "duration": total - 200}]
+        hps = {"lr": segs}
+        if momentum:
+            hps["momentum"] = [{"fn": {"family": "constant", "value": "0.9"}, "local_start": 0, "duration": total}]
+        out.append({"total_steps": total, "hps": hps})
+    return out
+
+
+def test_placement_splits_a_dominant_root():
+    from paper_2006_11972_b200 import host
+    trials = dominant_root_trials(momentum=False)
+    acts = [{"kind": "insert", "id": i, "study": 0, "trial": i, "config": c} for i, c in enumerate(trials)]
+    for G in (1, 2, 4, 8):
+        r = host.call({"op": "plan", "key": KEY_LR, "actions": acts, "placement": G})
+        place = {int(k): v for k, v in r["placement"].items()}
+        plan = json.loads(r["json"])
+        assert set(place) == {n["id"] for n in plan["nodes"]} and set(place.values()) <= set(range(G))
+        if G == 1:
+            assert set(place.values()) == {0}
+        else:  # the single root's subtree is split at its branch points over every device
+            assert len(set(place.values())) == G
+        # deterministic: same plan -> same placement
+        assert host.call({"op": "plan", "key": KEY_LR, "actions": acts, "placement": G})["placement"] == r["placement"]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_multi_device_engine_equals_single_device(seed):
+    """Engine(devices=[0, 0]) (two contexts): paths placed by subtree, split-off subtrees LOAD
+    through peer copies; every trial's metrics equal the single-device run's, no step re-run."""
+    rng = random.Random(900 + seed)
+    trials = dominant_root_trials() if seed % 3 == 0 else random_trials(rng)
+    one, _, s1 = run(trials, slots_per_gpu=4)
+    two, _, s2 = run(trials, slots_per_gpu=4, devices=[0, 0])
+    four, _, s4 = run(trials, slots_per_gpu=2, devices=[0, 0, 0, 0])
+    h1 = {t: one.history(*t) for t in one.trials()}
+    assert {t: two.history(*t) for t in two.trials()} == h1
+    assert {t: four.history(*t) for t in four.trials()} == h1
+    assert s1["stage_steps"] == s2["stage_steps"] == s4["stage_steps"]
+    if seed % 3 == 0:
+        assert s2["peer_copies"] > 0 and s4["peer_copies"] > 0
+
+
+def test_dominant_root_speeds_up_with_devices():
+    """Four GPUs x 2 slots vs one GPU x 2 slots on the dominant-root study: the makespan (max over
+    GPUs of their locksteps is bounded by the sum) drops; the work is spread over all devices."""
+    trials = dominant_root_trials()
+    e1, _, s1 = run(trials, slots_per_gpu=2)
+    e4, _, s4 = run(trials, slots_per_gpu=2, devices=[0, 0, 0, 0])
+    assert s4["peer_copies"] > 0
+    assert s4["model_wall_us"] < s1["model_wall_us"]
