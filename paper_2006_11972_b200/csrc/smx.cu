@@ -967,25 +967,46 @@ int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
         check_ckpt(dst, dst_ckpt);
         check_ckpt(src, src_ckpt);
         if (!src->ck_valid[src_ckpt]) fail(SMX_EINTEGRITY, "peer copy from empty checkpoint entry");
+        if (dst->palloc != src->palloc) fail(SMX_ECONFIG, "peer copy between different models");
         ck(cudaStreamSynchronize(src->stream), "src sync");
         cudaSetDevice(dst->device);
-        const size_t bytes = sizeof(float) * dst->slab_stride();
-        if (dst->device != src->device) {
+        bool direct = dst->device == src->device;
+        if (!direct) {
             int can = 0;
             ck(cudaDeviceCanAccessPeer(&can, dst->device, src->device), "can access peer");
             if (can) {
                 cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
                 cudaGetLastError();
+                direct = true;
             }
         }
-        if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
-        ck(cudaMemcpyPeerAsync(dst->pool + dst->slab_stride() * dst_ckpt, dst->device,
-                               src->pool + src->slab_stride() * src_ckpt, src->device, bytes, dst->stream),
-           "peer copy");
-        ck(cudaMemcpyPeerAsync(dst->ck_st + dst_ckpt, dst->device, src->ck_st + src_ckpt, src->device,
-                               sizeof(SlotState), dst->stream),
-           "peer state copy");
+        if (direct) {
+            // K7 = the K6 fork kernel on the destination GPU reading the source pool through
+            // NVLink peer loads (unified addressing): one launch, w | m and the slot state
+            CopyJob j{reinterpret_cast<const float4*>(src->pool + src->slab_stride() * src_ckpt),
+                      reinterpret_cast<float4*>(dst->pool + dst->slab_stride() * dst_ckpt), src->ck_st + src_ckpt,
+                      dst->ck_st + dst_ckpt};
+            if (!dst->jobs || dst->jobs_cap < 1) {
+                if (dst->jobs) cudaFree(dst->jobs);
+                dst->jobs_cap = 2;
+                ck(cudaMalloc(&dst->jobs, sizeof(CopyJob) * dst->jobs_cap), "cudaMalloc jobs");
+            }
+            ck(cudaMemcpyAsync(dst->jobs, &j, sizeof j, cudaMemcpyHostToDevice, dst->stream), "job H2D");
+            const long long n4 = 2 * dst->palloc / 4;
+            if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
+            fork_copy_kernel<<<dim3(fork_blocks(n4), 1), 256, 0, dst->stream>>>(dst->jobs, n4);
+            launch_check(dst, "peer fork_copy");
+        } else {  // no peer access between these GPUs: the runtime's staged peer copy
+            if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
+            const size_t bytes = sizeof(float) * dst->slab_stride();
+            ck(cudaMemcpyPeerAsync(dst->pool + dst->slab_stride() * dst_ckpt, dst->device,
+                                   src->pool + src->slab_stride() * src_ckpt, src->device, bytes, dst->stream),
+               "peer copy");
+            ck(cudaMemcpyPeerAsync(dst->ck_st + dst_ckpt, dst->device, src->ck_st + src_ckpt, src->device,
+                                   sizeof(SlotState), dst->stream),
+               "peer state copy");
+        }
         if (dst->timing) {
             cudaEventRecord(dst->ev[5], dst->stream);
             cudaEventSynchronize(dst->ev[5]);
