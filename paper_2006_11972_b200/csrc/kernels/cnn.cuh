@@ -140,7 +140,10 @@ inline ActLayout act_layout(int max_batch) {
 // stride of 2), the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients, and
 // the weight gradients' im2col operands (a1 / a2 again, one box of 32 output pixels x all input
 // channels per tap).
-enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmapKinds = 6 };
+enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmWgB2 = 6, kTmWgB3 = 7, kTmapKinds = 8 };
+// kTmWgB2 / kTmWgB3: the weight gradients' B operand (the layer's output gradient d2 / d3 as a
+// 2-D [sample x pixel][Co] tensor): 32 x 32 boxes with the 128-byte / 32-byte-atom swizzle = the
+// UMMA MN-major tf32 layout (SWIZZLE_128B_BASE32B), loaded straight into the B stage.
 
 struct ConvArgs {
     const int* slots;
@@ -478,7 +481,7 @@ template <int L>
 struct Fwd {
     using G = Geo<L>;
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiBiasRelu, kMaxN = G::Co;
-    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true;
+    static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = true, B_TMA = false;
     static constexpr bool A_TMA = (L >= 2);  // A tile = one strided TMA box per chunk
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = L == 3 ? 8 : 4;
     static constexpr int kRowsPerSample = G::OH * G::OH;
@@ -588,7 +591,7 @@ struct Dgrad {
     using G = Geo<L>;
     static_assert(G::S == 2, "sub-pixel decomposition is for stride 2");
     static constexpr int AM = 0, BMODE = 0, EPI = kEpiMask, kMaxN = WImg<L>::DgrNTile;
-    static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true;
+    static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true, B_TMA = false;
     static constexpr bool A_TMA = true;  // A tile = one shifted TMA box of dy per chunk
     static constexpr bool kInMaskBits = false, kMaskFromBits = true, kSgd = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
@@ -678,6 +681,9 @@ struct Wgrad {
     using G = Geo<L>;
     static constexpr int AM = 1, BMODE = 1, EPI = kEpiPartT, kMaxN = G::Co;
     static constexpr bool A_EXACT = (L == 1), B_EXACT = false, B_IMAGE = false, A_TMA = (L >= 2);
+    // B = dY[m][co] (co contiguous: MN-major) by TMA, 32 co x 32 m boxes (SWIZZLE_128B_BASE32B)
+    static constexpr bool B_TMA = (L >= 2);
+    const CUtensorMap* btmap;
     static constexpr bool kInMaskBits = false, kMaskFromBits = false, kSgd = false;
     // TMA: a tile's 128 rows are 128 / Ci taps x Ci channels; one box per tap = 32 output pixels
     // (the chunk's reduction indices) x Ci channels, stored [tap][pixel][ci]
@@ -744,6 +750,7 @@ struct Wgrad {
         in = layer_in<L>(p, v);
         dy = layer_dout<L>(p, v);
         tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmWg3 : kTmWg2);
+        btmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmWgB3 : kTmWgB2);
         part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3);
         const int total = v.bs * G::OH * G::OH;
         split = s;

@@ -52,14 +52,15 @@ struct WsPlan {
                                                                     // XOR-swizzled by row
     // masked epilogues reading the ReLU mask as a bitmap stage the tile's words in shared memory
     static constexpr int MaskWords = (Op::EPI == 1 && Op::kMaskFromBits) ? kBM * N / 32 : 0;
-    static constexpr int Fixed = Stages * BStage + 256 + Sacc + MaskWords * 4;
+    static constexpr int BarBytes = 512;
+    static constexpr int Fixed = Stages * BStage + BarBytes + Sacc + MaskWords * 4;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
     // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
     static constexpr int ARaw = (ARawMax > 8 ? 8 : ARawMax) & ~1;
     static_assert(ARaw >= 4, "shared memory plan");
     static constexpr int ARawOff = Stages * BStage;
     static constexpr int BarOff = ARawOff + ARaw * kARawTile;
-    static constexpr int SaccOff = BarOff + 256;
+    static constexpr int SaccOff = BarOff + BarBytes;
     static constexpr int MbitsOff = SaccOff + Sacc;
     static constexpr int Bytes = MbitsOff + MaskWords * 4;
     // epilogue: one warp per TMEM lane quadrant (4), or two each draining half the columns (8)
@@ -70,7 +71,10 @@ struct WsPlan {
     // TMA A operands: one more warp whose elected lane streams the A boxes of every chunk into the
     // raw ring as soon as the group that read a slot has released it
     static constexpr int TmaWarp = Op::A_TMA ? MmaWarp + 1 : -1;
-    static constexpr int Threads = (MmaWarp + (Op::A_TMA ? 2 : 1)) * 32;
+    // TMA B operands (Op::B_TMA): one more warp whose elected lane loads each chunk's B tile
+    // straight into its stage as soon as the stage's previous MMAs are done
+    static constexpr int BTmaWarp = Op::B_TMA ? MmaWarp + 1 + (Op::A_TMA ? 1 : 0) : -1;
+    static constexpr int Threads = (MmaWarp + 1 + (Op::A_TMA ? 1 : 0) + (Op::B_TMA ? 1 : 0)) * 32;
 };
 template <class Op>
 constexpr int ws_smem() {
@@ -174,7 +178,8 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
     uint64_t* acce = accf + 2;
     uint64_t* rawf = acce + 2;  // TMA A operands: raw slot filled (expect_tx) / released by the group's 4 warps
     uint64_t* rawe = rawf + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawe + 8);
+    uint64_t* bfull = rawe + 8;  // TMA B operands: the stage's hi tile landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + kMaxStages);
 
     Op op;
     op.setup(p, blockIdx.z, blockIdx.x);
@@ -210,6 +215,8 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 mbar_init(&rawf[r], 1);
                 mbar_init(&rawe[r], 4);
             }
+        if constexpr (Op::B_TMA)
+            for (int st = 0; st < kStages; ++st) mbar_init(&bfull[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     const int uu = gt + j * 128, r = uu % nt, kq = uu / nt, k = k0 + kq * 4;
                     b[j] = ld4(kq < kKQ && r < N && k < klim ? op.b_ptr(r, k) : nullptr);
                 }
-            } else if constexpr (!Op::B_IMAGE && !kDbgNoBreg) {
+            } else if constexpr (!Op::B_IMAGE && !Op::B_TMA && !kDbgNoBreg) {
                 // MN-contiguous B: unit (row r, k quad) = 4 scalar loads down the reduction index;
                 // lanes = consecutive rows, so each load is one coalesced 128-byte line and the
                 // unit is already the K-major 16-byte group (no transpose)
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 }
             }
             // warm L2 with the B rows of this group's chunk kDw + 1 ahead (register-path B)
-            if constexpr (!Op::B_IMAGE) {
+            if constexpr (!Op::B_IMAGE && !Op::B_TMA) {
                 int pc = c + 2 * (kDw + 1);
                 while (pc >= nchunks) pc -= nchunks;
                 if (g + 2 * (kDw + 1) < total) {
@@ -433,6 +440,18 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
 #endif
             // B hi/lo -> smem canonical
             if constexpr (kDbgNoBreg) {
+            } else if constexpr (Op::B_TMA) {
+                // the TMA wrote the hi tile (the fp32 values: the MMA truncates them to tf32) in
+                // the MN-major 128B/32B-atom swizzled layout; lo = b - trunc(b) element by
+                // element lands at the same (swizzled) positions of the lo tile
+                mbar_wait(&bfull[s], u & 1);
+                const float4* hi4 = reinterpret_cast<const float4*>(bh);
+                float4* lo4 = reinterpret_cast<float4*>(bl);
+#pragma unroll 4
+                for (int j = gt; j < nt * kKC / 4; j += 128) {
+                    const float4 v = hi4[j];
+                    lo4[j] = make_float4(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w));
+                }
             } else if constexpr (!Op::B_IMAGE) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -491,10 +510,35 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             }
             __syncwarp();
         }
+    } else if (warp == Plan::BTmaWarp) {
+        // ================= TMA producer of the B operands (one elected lane) =================
+        // chunk g's B tile (nt channels x 32 reduction rows, nt / 32 swizzled 4 KB boxes) goes to
+        // stage g % kStages once the MMAs of the stage's previous chunk have completed
+        if constexpr (Op::B_TMA) {
+            if (lane == 0) {
+                int c = 0;
+                for (int g = 0; g < total; ++g) {
+                    const int s = g % kStages, u = g / kStages;
+                    if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                    const uint32_t bar = smem_u32(&bfull[s]), dst = smem_u32(smem + s * kBStage);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nt * kKC * 4));
+                    const int row = op.kbeg + c * kKC;
+                    for (int b = 0; b < nt / 32; ++b)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + b * 4096),
+                            "l"(op.btmap), "r"(32 * b), "r"(row), "r"(bar)
+                            : "memory");
+                    if (++c == nchunks) c = 0;
+                }
+            }
+            __syncwarp();
+        }
     } else if (warp == Plan::MmaWarp) {
         // ================= MMA issuer (whole warp, elected lane issues) =================
         {
-            const uint32_t idesc = idesc_tf32(nt);
+            // TMA B operands are MN-major (instruction descriptor bit 16)
+            const uint32_t idesc = idesc_tf32(nt) | (Op::B_TMA ? (1u << 16) : 0u);
             const uint32_t smem_base = smem_u32(smem);
             int g = 0, un = 0;
             for (int i = 0; i < ntiles; ++i) {
@@ -520,8 +564,11 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
                     // descriptors built once per chunk; a k-step of 8 tf32 advances the B tiles by
                     // 2 LBO (the 14-bit address field cannot overflow below 256 KB of smem)
-                    const uint64_t dbh0 = smem_desc(bhi, lbo, 128), dbl0 = smem_desc(blo, lbo, 128);
-                    const uint64_t dstep = (uint64_t)((2 * lbo) >> 4);
+                    // (TMA B: MN-major SWIZZLE_128B_BASE32B -- LBO = 4 KB between 32-column atoms,
+                    // SBO = 512 B between 4-row k groups; a k-step of 8 rows advances 1 KB)
+                    const uint64_t dbh0 = Op::B_TMA ? smem_desc_mn32(bhi, 4096, 512) : smem_desc(bhi, lbo, 128);
+                    const uint64_t dbl0 = Op::B_TMA ? smem_desc_mn32(blo, 4096, 512) : smem_desc(blo, lbo, 128);
+                    const uint64_t dstep = Op::B_TMA ? (uint64_t)(1024 >> 4) : (uint64_t)((2 * lbo) >> 4);
 #ifndef SMX_DBG_NO_MMA
                     if (ksteps == 4) {
 #pragma unroll

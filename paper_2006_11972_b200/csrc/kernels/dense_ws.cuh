@@ -25,7 +25,8 @@ template <int AM_, int BM_, int EPI_, bool AX, bool BX, bool SGD = false>
 struct DenseOp {
     using Args = GemmArgs;
     static constexpr int AM = AM_, BMODE = BM_, EPI = EPI_, kMaxN = 128;
-    static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false;
+    static constexpr bool A_EXACT = AX, B_EXACT = BX, B_IMAGE = false, A_TMA = false, B_TMA = false;
+    const CUtensorMap* btmap = nullptr;
     static constexpr int kBoxes = 1, kTmaCi = 1;
     static constexpr bool kInMaskBits = false, kMaskFromBits = false, kSgd = SGD;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 4;

@@ -123,6 +123,16 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
+// UMMA shared-memory descriptor of an MN-major tf32 operand.  tf32 MN-major operands have one
+// shared-memory layout, SWIZZLE_128B_BASE32B (layout type 1): 128-byte rows (32 elements along
+// MN, one k each), 32-byte granules XOR-swizzled by (row % 4) -- what a TMA box with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes.  LBO = distance between 32-element atom columns
+// along MN, SBO = distance between 4-row groups along K.  Verified by profiles/micro/mnmajor_test.cu.
+__device__ __forceinline__ uint64_t smem_desc_mn32(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (1ull << 61);
+}
+
 // Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
 __device__ __forceinline__ uint32_t idesc_tf32(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);

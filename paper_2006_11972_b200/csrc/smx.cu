@@ -211,7 +211,7 @@ void make_conv_tmaps(smx_ctx* c) {
         int C, W, H, n_box, w_box, h_box, stride;  // box: 32 (conv2 / conv3 A tiles) or C channels x w_box x h_box x n_box
     };
     const long long mb = c->d.max_batch;
-    const Spec specs[cnn::kTmapKinds] = {
+    const Spec specs[cnn::kTmWgB2] = {
         {c->al.a1, 32, 32, 32, 1, 16, 8, 2},   // conv2 forward: a1, output tile = 8 rows x 16 columns
         {c->al.a2, 64, 16, 16, 2, 8, 8, 2},    // conv3 forward: a2, 2 samples x 8 x 8
         {c->al.d2, 64, 16, 16, 1, 16, 8, 1},   // conv2 input gradient: d2, 8 x 16 blocks
@@ -221,7 +221,7 @@ void make_conv_tmaps(smx_ctx* c) {
     };
     std::vector<CUtensorMap> h((size_t)c->S * cnn::kTmapKinds);
     for (int s = 0; s < c->S; ++s)
-        for (int k = 0; k < cnn::kTmapKinds; ++k) {
+        for (int k = 0; k < cnn::kTmWgB2; ++k) {
             const Spec& sp = specs[k];
             float* base = c->act + c->act_stride * s + sp.off;
             const cuuint64_t dims[4] = {(cuuint64_t)sp.C, (cuuint64_t)sp.W, (cuuint64_t)sp.H, (cuuint64_t)mb};
@@ -236,6 +236,23 @@ void make_conv_tmaps(smx_ctx* c) {
                                    wg ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        }
+    // the weight gradients' B operands: d2 / d3 as 2-D [max_batch x pixels][Co] tensors, boxes of
+    // 32 channels (128 bytes) x 32 reduction rows with the 128-byte / 32-byte-atom swizzle (the
+    // UMMA MN-major tf32 layout SWIZZLE_128B_BASE32B)
+    for (int s = 0; s < c->S; ++s)
+        for (int L = 2; L <= 3; ++L) {
+            const int C = L == 2 ? 64 : 128, pix = L == 2 ? 256 : 64;
+            float* base = c->act + c->act_stride * s + (L == 2 ? c->al.d2 : c->al.d3);
+            const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)(mb * pix)};
+            const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
+            const cuuint32_t box[2] = {32, 32};
+            const cuuint32_t es[2] = {1, 1};
+            const int k = L == 2 ? cnn::kTmWgB2 : cnn::kTmWgB3;
+            const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (B) failed (" + std::to_string((int)r) + ")");
         }
     ck(cudaMalloc(&c->tmaps, sizeof(CUtensorMap) * h.size()), "tensor maps");
     ck(cudaMemcpy(c->tmaps, h.data(), sizeof(CUtensorMap) * h.size(), cudaMemcpyHostToDevice), "tensor maps H2D");
