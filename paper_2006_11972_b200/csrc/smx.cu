@@ -26,6 +26,7 @@
 #include "kernels/cnn.cuh"
 #include "kernels/conv_ws.cuh"
 #include "kernels/dense_ws.cuh"
+#include "kernels/wgrad2_at.cuh"
 
 using namespace smx;
 
@@ -216,7 +217,7 @@ void make_conv_tmaps(smx_ctx* c) {
         {c->al.a2, 64, 16, 16, 2, 8, 8, 2},    // conv3 forward: a2, 2 samples x 8 x 8
         {c->al.d2, 64, 16, 16, 1, 16, 8, 1},   // conv2 input gradient: d2, 8 x 16 blocks
         {c->al.d3, 128, 8, 8, 2, 8, 8, 1},     // conv3 input gradient: d3, 2 samples x 8 x 8 blocks
-        {c->al.a1, 32, 32, 32, 1, 16, 2, 2},   // conv2 weight gradient: a1, 32 output pixels (2 x 16) per tap
+        {c->al.a1, 32, 32, 32, 1, 33, 5, 1},   // conv2 weight gradient: a1 window of 32 output pixels (2 x 16), all taps
         {c->al.a2, 64, 16, 16, 1, 8, 4, 2},    // conv3 weight gradient: a2, 32 output pixels (4 x 8) per tap
     };
     std::vector<CUtensorMap> h((size_t)c->S * cnn::kTmapKinds);
@@ -309,6 +310,19 @@ void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) 
     launch_check(c, "conv_ws");
 }
 
+// conv2 weight gradient, all taps per CTA (kernels/wgrad2_at.cuh): one CTA per (2048-pixel split, slot)
+void wgrad2_at(smx_ctx* c, const cnn::ConvArgs& a, int splits, int groups) {
+    static unsigned long long configured = 0;
+    const unsigned long long bit = 1ull << (c->device & 63);
+    if (!(configured & bit)) {
+        ck(cudaFuncSetAttribute(cnn::wg2::wgrad2_at_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cnn::wg2::kSmem),
+           "wgrad2_at smem attribute");
+        configured |= bit;
+    }
+    cnn::wg2::wgrad2_at_kernel<<<dim3(splits, 1, groups), cnn::wg2::kThreads, cnn::wg2::kSmem, c->cur>>>(a);
+    launch_check(c, "wgrad2_at");
+}
+
 template <int L>
 void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
@@ -338,7 +352,10 @@ void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
         const int splits = (mb * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
-        conv_tc<cnn::ctc::Wgrad<L>>(c, a, splits, cnn::Part<L>::Rows, n);
+        if constexpr (L == 2)
+            wgrad2_at(c, a, splits, n);
+        else
+            conv_tc<cnn::ctc::Wgrad<L>>(c, a, splits, cnn::Part<L>::Rows, n);
         const int fc = (L == 3 && a.fuse_update) ? cnn::kFcBlocks : 0;  // + the FC layer's update
         cnn::wgrad_reduce_kernel<L><<<dim3(G::Co + fc, n), 128, 0, c->cur>>>(a);
         launch_check(c, "wgrad_reduce");
@@ -1311,7 +1328,7 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
                 } else if (c->d.gemm_mode == SMX_GEMM_TC) {  // the implicit GEMM alone (no split reduction)
                     using G = cnn::Geo<2>;
                     const int splits = (c->d.max_batch * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
-                    conv_tc<cnn::ctc::Wgrad<2>>(c, a, splits, cnn::Part<2>::Rows, n);
+                    wgrad2_at(c, a, splits, n);
                 } else {
                     conv_wgrad<2>(c, a, n, c->d.max_batch);
                 }
