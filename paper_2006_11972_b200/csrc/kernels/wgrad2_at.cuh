@@ -14,13 +14,13 @@
 //     TMA warp   one 4-D box of the chunk's input window (5 input rows x 33 columns (-1..31) x
 //                32 channels, zero fill = the convolution's padding; 21 KB) + the d2 tile (two
 //                32 x 32 MN-major 128B/32B-atom swizzled boxes, 8 KB) into the stage
-//     producers  (warps 0-3, warp q = TMEM lane quadrant q): B lo = b - trunc(b) in place next to
-//                the TMA'd hi tile; then for each M tile t the im2col rows of tap 4t + q (lane =
+//     producers  (warps 0-3, warp q = TMEM lane quadrant q): for each M tile t the im2col rows of tap 4t + q (lane =
 //                input channel) straight from the window (input (2r + kh, 2ow + kw) for pixel
 //                (r, ow): one conflict-free LDS per k), split hi / lo, tcgen05.st to a TMEM A slot
 //                (5-slot ring; tile 2 quadrant 1 lane 0 = the all-ones bias row)
 //     MMA warp   per tile 4 k-steps x 3 kind::tf32 MMAs (3xTF32) into the tile's accumulator
-//     epilogue   (warps 4-13, one per lane quadrant holding outputs): every 4 chunks drain the tile's accumulator and
+//     epilogue   (warps 4-13, one per lane quadrant holding outputs; warps 4-11 also write B lo =
+//                b - trunc(b) next to the TMA'd hi tile): every 4 chunks drain the tile's accumulator and
 //                add it into fp32 register sums (round-to-nearest, fixed order: §3b.5), write the
 //                tile's partial rows at the end
 //   = 29 KB of L2 traffic and ~150 KB of shared-memory traffic per 36 MMAs.
@@ -52,18 +52,35 @@ constexpr int kWinBytes = kWinRows * kWinCols * G::Ci * 4;         // 21120
 constexpr int kBBytes = 32 * G::Co * 4;                            // 8192 (hi or lo)
 constexpr int kStageBytes = (2 * kBBytes + kWinBytes + 1023) / 1024 * 1024;  // 37888
 constexpr int kBarOff = kStages * kStageBytes;
-constexpr int kSmem = kBarOff + 256;
+constexpr int kSmem = kBarOff + 512;
 constexpr int kASlots = 5;
 constexpr int kAccCols = 64, kABase = 3 * kAccCols;
 // warps: 0-3 producers, 4-7 / 8-11 epilogue of tiles 0 / 1, 12-13 epilogue of tile 2 (only its lane
 // quadrants 0 (tap 8) and 1 (the bias row) hold outputs), 14 MMA, 15 TMA: 16 warps = 128 registers
 constexpr int kProdWarps = 4, kEpiWarp0 = 4, kMmaWarp = 14, kTmaWarp = 15;
+constexpr int kBloThreads = 256;  // the epilogue warps of tiles 0 / 1 also split each chunk's B tile
 constexpr int kThreads = 16 * 32;
 constexpr int kSeg = SMX_SEG_CHUNKS;
 static_assert(kABase + kASlots * 64 == 512, "TMEM plan");
 static_assert(kSmem <= 227 * 1024, "shared-memory plan");
 
-__global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p) {
+// A work item = (slot, 2048-pixel split); the grid is persistent (one CTA per SM) and CTA b takes
+// items b, b + gridDim.x, ...  Every role walks the same item sequence; chunk and segment counters
+// run on across items, so the pipeline never drains between them.
+struct Item {
+    int slot, split, kbeg, nchunks;
+};
+__device__ __forceinline__ bool item_at(const ConvArgs& p, int j, int splits, Item& it) {
+    const int z = j / splits;
+    it.split = j % splits;
+    it.slot = p.slots[z];
+    const int total = conv_bs(p, it.slot) * G::OH * G::OH;  // a multiple of 256
+    it.kbeg = it.split * kSplitRows;
+    it.nchunks = min(kSplitRows, total - it.kbeg) / 32;
+    return it.nchunks > 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p, int splits, int nitems) {
     extern __shared__ __align__(1024) char smem[];
     uint64_t* tfull = reinterpret_cast<uint64_t*>(smem + kBarOff);  // stage landed (TMA tx)
     uint64_t* empty = tfull + kStages;                              // stage's MMAs done
@@ -71,16 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p) {
     uint64_t* aempty = afull + kASlots;                             // A slot's MMAs done
     uint64_t* accf = aempty + kASlots;                              // tile accumulator segment done
     uint64_t* acce = accf + 3;                                      // tile accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 3);
-
-    const SlotView v = slot_view(p, p.slots[blockIdx.z]);
-    const int split = blockIdx.x;
-    const int total = v.bs * G::OH * G::OH;
-    const int kbeg = split * kSplitRows;
-    const int K = min(kSplitRows, total - kbeg);
-    if (K <= 0) return;
-    const int nchunks = K / 32;  // total is a multiple of 256
-    const int nseg = (nchunks + kSeg - 1) / kSeg;
+    uint64_t* bready = acce + 3;                                    // stage's B lo written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + kStages);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0) {
@@ -92,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&tfull[s], 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&bready[s], kBloThreads);
         }
         for (int a = 0; a < kASlots; ++a) {
             mbar_init(&afull[a], kProdWarps * 32);
@@ -107,143 +117,190 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    Item it;
 
     if (warp < kProdWarps) {
         // ================= producers =================
         const int q = warp;
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-        for (int g = 0; g < nchunks; ++g) {
-            const int s = g % kStages;
-            mbar_wait(&tfull[s], (g / kStages) & 1);
-            char* st = smem + s * kStageBytes;
-            {  // B lo next to the TMA'd hi tile (same swizzled positions)
-                const float4* hi4 = reinterpret_cast<const float4*>(st);
-                float4* lo4 = reinterpret_cast<float4*>(st + kBBytes);
-#pragma unroll
-                for (int j = threadIdx.x; j < kBBytes / 16; j += kProdWarps * 32) {
-                    const float4 b = hi4[j];
-                    lo4[j] = make_float4(lo_of(b.x), lo_of(b.y), lo_of(b.z), lo_of(b.w));
-                }
-            }
-            const float* win = reinterpret_cast<const float*>(st + 2 * kBBytes);
+        int gg = 0;  // chunks processed by this CTA
+        for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
+            if (!item_at(p, j, splits, it)) continue;
+            for (int g = 0; g < it.nchunks; ++g, ++gg) {
+                const int s = gg % kStages;
+                mbar_wait(&tfull[s], (gg / kStages) & 1);
+                char* st = smem + s * kStageBytes;
+                const float* win = reinterpret_cast<const float*>(st + 2 * kBBytes);
 #pragma unroll 1
-            for (int t = 0; t < 3; ++t) {
-                const int i = 3 * g + t, a = i % kASlots;
-                if (i >= kASlots) mbar_wait(&aempty[a], ((i / kASlots) - 1) & 1);
-                const int tap = 4 * t + q;
-                const uint32_t ta = tq + kABase + a * 64;
-                if (tap < 9) {
-                    const float* src = win + ((tap / 3) * kWinCols + tap % 3) * G::Ci + lane;
-                    float x[32];
+                for (int t = 0; t < 3; ++t) {
+                    const int i = 3 * gg + t, a = i % kASlots;
+                    if (i >= kASlots) mbar_wait(&aempty[a], ((i / kASlots) - 1) & 1);
+                    const int tap = 4 * t + q;
+                    const uint32_t ta = tq + kABase + a * 64;
+                    if (tap < 9) {
+                        const float* src = win + ((tap / 3) * kWinCols + tap % 3) * G::Ci + lane;
+                        float x[32];
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) x[k] = src[((k >> 4) * 2 * kWinCols + 2 * (k & 15)) * G::Ci];
-                    tmem_st16(ta, x);
-                    tmem_st16(ta + 16, x + 16);
-                    float lo[32];
+                        for (int k = 0; k < 32; ++k) {
+#ifdef WG2_DBG_NO_WIN  // profiling variant: no window reads
+                            x[k] = __int_as_float(0x3f000000 + lane + k);
+#else
+                            x[k] = src[((k >> 4) * 2 * kWinCols + 2 * (k & 15)) * G::Ci];
+#endif
+                        }
+                        tmem_st16(ta, x);
+                        tmem_st16(ta + 16, x + 16);
+                        float lo[32];
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) lo[k] = lo_of(x[k]);
-                    tmem_st16(ta + 32, lo);
-                    tmem_st16(ta + 48, lo + 16);
-                } else if (tap == 9) {  // tile 2, quadrant 1: row 288 = the all-ones bias row
-                    float x[16], z[16];
+                        for (int k = 0; k < 32; ++k) lo[k] = lo_of(x[k]);
+                        tmem_st16(ta + 32, lo);
+                        tmem_st16(ta + 48, lo + 16);
+                    } else if (tap == 9) {  // tile 2, quadrant 1: row 288 = the all-ones bias row
+                        float x[16], z[16];
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        x[k] = lane == 0 ? 1.0f : 0.0f;
-                        z[k] = 0.0f;
-                    }
-                    tmem_st16(ta, x);
-                    tmem_st16(ta + 16, x);
-                    tmem_st16(ta + 32, z);
-                    tmem_st16(ta + 48, z);
-                }  // quadrants 2, 3 of tile 2: padding rows, never stored
-                asm volatile("tcgen05.wait::st.sync.aligned;");
-                if (t == 0) asm volatile("fence.proxy.async.shared::cta;");  // B lo -> the MMA's async proxy
-                asm volatile("tcgen05.fence::before_thread_sync;");
-                mbar_arrive(&afull[a]);
+                        for (int k = 0; k < 16; ++k) {
+                            x[k] = lane == 0 ? 1.0f : 0.0f;
+                            z[k] = 0.0f;
+                        }
+                        tmem_st16(ta, x);
+                        tmem_st16(ta + 16, x);
+                        tmem_st16(ta + 32, z);
+                        tmem_st16(ta + 48, z);
+                    }  // quadrants 2, 3 of tile 2: padding rows, never stored
+                    asm volatile("tcgen05.wait::st.sync.aligned;");
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&afull[a]);
+                }
             }
         }
     } else if (warp == kTmaWarp) {
         // ================= TMA producer (one elected lane) =================
         if (lane == 0) {
-            const CUtensorMap* wmap = p.tmaps + (long long)v.slot * kTmapKinds + kTmWg2;
-            const CUtensorMap* bmap = p.tmaps + (long long)v.slot * kTmapKinds + kTmWgB2;
-            for (int g = 0; g < nchunks; ++g) {
-                const int s = g % kStages;
-                if (g >= kStages) mbar_wait(&empty[s], ((g / kStages) - 1) & 1);
-                const uint32_t bar = smem_u32(&tfull[s]), dst = smem_u32(smem + s * kStageBytes);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                             "r"(2 * 4096 + kWinBytes));
-                const int pix = kbeg + 32 * g;
-                const int n = pix / (G::OH * G::OH), oh0 = (pix % (G::OH * G::OH)) / G::OH;
-                for (int b = 0; b < 2; ++b)
+            int gg = 0;
+            for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
+                if (!item_at(p, j, splits, it)) continue;
+                const CUtensorMap* wmap = p.tmaps + (long long)it.slot * kTmapKinds + kTmWg2;
+                const CUtensorMap* bmap = p.tmaps + (long long)it.slot * kTmapKinds + kTmWgB2;
+                for (int g = 0; g < it.nchunks; ++g, ++gg) {
+                    const int s = gg % kStages;
+                    if (gg >= kStages) mbar_wait(&empty[s], ((gg / kStages) - 1) & 1);
+                    const uint32_t bar = smem_u32(&tfull[s]), dst = smem_u32(smem + s * kStageBytes);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                 "r"(2 * 4096 + kWinBytes));
+                    const int pix = it.kbeg + 32 * g;
+                    const int n = pix / (G::OH * G::OH), oh0 = (pix % (G::OH * G::OH)) / G::OH;
+                    for (int b = 0; b < 2; ++b)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + b * 4096),
+                            "l"(bmap), "r"(32 * b), "r"(pix), "r"(bar)
+                            : "memory");
                     asm volatile(
-                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + b * 4096),
-                        "l"(bmap), "r"(32 * b), "r"(pix), "r"(bar)
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + 2 * kBBytes),
+                        "l"(wmap), "r"(0), "r"(-1), "r"(2 * oh0 - 1), "r"(n), "r"(bar)
                         : "memory");
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst + 2 * kBBytes),
-                    "l"(wmap), "r"(0), "r"(-1), "r"(2 * oh0 - 1), "r"(n), "r"(bar)
-                    : "memory");
+                }
             }
         }
         __syncwarp();
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer (whole warp, elected lane issues) =================
         const uint32_t idesc = idesc_tf32(G::Co) | (1u << 16);  // B MN-major
-        for (int g = 0; g < nchunks; ++g) {
-            const int s = g % kStages;
-            const bool seg_start = g % kSeg == 0, seg_end = g % kSeg == kSeg - 1 || g == nchunks - 1;
-            const uint32_t bhi = smem_u32(smem + s * kStageBytes), blo = bhi + kBBytes;
-            const uint64_t dbh0 = smem_desc_mn32(bhi, 4096, 512), dbl0 = smem_desc_mn32(blo, 4096, 512);
-            constexpr uint64_t kStep = 1024 >> 4;  // a k-step of 8 MN-major rows
-            for (int t = 0; t < 3; ++t) {
-                const int i = 3 * g + t, a = i % kASlots;
-                if (seg_start && g > 0) mbar_wait(&acce[t], ((g / kSeg) - 1) & 1);
-                mbar_wait(&afull[a], (i / kASlots) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t dacc = tmem + t * kAccCols, ahi = tmem + kABase + a * 64, alo = ahi + 32;
+        int gg = 0, sg = 0;  // chunks / accumulation segments started by this CTA
+        for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
+            if (!item_at(p, j, splits, it)) continue;
+            for (int g = 0; g < it.nchunks; ++g, ++gg) {
+                const int s = gg % kStages;
+                const bool seg_start = g % kSeg == 0, seg_end = g % kSeg == kSeg - 1 || g == it.nchunks - 1;
+                const uint32_t bhi = smem_u32(smem + s * kStageBytes), blo = bhi + kBBytes;
+                const uint64_t dbh0 = smem_desc_mn32(bhi, 4096, 512), dbl0 = smem_desc_mn32(blo, 4096, 512);
+                constexpr uint64_t kStep = 1024 >> 4;  // a k-step of 8 MN-major rows
+                for (int t = 0; t < 3; ++t) {
+                    const int i = 3 * gg + t, a = i % kASlots;
+                    if (seg_start && sg > 0) mbar_wait(&acce[t], (sg - 1) & 1);
+                    if (t == 0) mbar_wait(&bready[s], (gg / kStages) & 1);
+                    mbar_wait(&afull[a], (i / kASlots) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t dacc = tmem + t * kAccCols, ahi = tmem + kABase + a * 64, alo = ahi + 32;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    mma_ts_e(dacc, alo + 8 * k, dbh0 + k * kStep, idesc, (seg_start && k == 0) ? 0u : 1u);
-                    mma_ts_e(dacc, ahi + 8 * k, dbl0 + k * kStep, idesc, 1u);
-                    mma_ts_e(dacc, ahi + 8 * k, dbh0 + k * kStep, idesc, 1u);
+                    for (int k = 0; k < 4; ++k) {
+#ifndef WG2_DBG_NO_LO  // profiling variant: 2 MMAs per k-step
+                        mma_ts_e(dacc, alo + 8 * k, dbh0 + k * kStep, idesc, (seg_start && k == 0) ? 0u : 1u);
+#endif
+                        mma_ts_e(dacc, ahi + 8 * k, dbl0 + k * kStep, idesc, 1u);
+                        mma_ts_e(dacc, ahi + 8 * k, dbh0 + k * kStep, idesc, 1u);
+                    }
+                    mma_commit_e(&aempty[a]);
+                    if (seg_end) mma_commit_e(&accf[t]);
                 }
-                mma_commit_e(&aempty[a]);
-                if (seg_end) mma_commit_e(&accf[t]);
+                mma_commit_e(&empty[s]);
+                if (seg_end) ++sg;
             }
-            mma_commit_e(&empty[s]);
         }
         __syncwarp();
     } else {
         // ================= epilogue: one warp per lane quadrant holding outputs =================
+        // The warps of tiles 0 / 1 also write each chunk's B lo (= b - trunc(b) at the TMA'd hi
+        // tile's swizzled positions), one chunk ahead of the drains, so a drain never holds up
+        // the next chunk's MMAs.
         const int t = (warp - kEpiWarp0) >> 2, q = warp & 3;
         const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + t * kAccCols;
-        float sum[64];
-        for (int j = 0; j < nseg; ++j) {
-            mbar_wait(&accf[t], j & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t r[32];
-                tmem_ld16(tacc + 32 * h, r);
-                tmem_ld16(tacc + 32 * h + 16, r + 16);
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-                if (h == 1) {
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&acce[t]);
-                }
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    sum[32 * h + c] = j == 0 ? __uint_as_float(r[c]) : __fadd_rn(sum[32 * h + c], __uint_as_float(r[c]));
-            }
-        }
         const int m = 128 * t + 32 * q + lane;
-        if (m < Part<2>::Rows) {
-            float* out = v.act + p.al.p2 + (long long)split * G::Co * Part<2>::Ld + m;
+        const bool blo_role = t < 2;
+        const int bt = threadIdx.x - kEpiWarp0 * 32;
+        int total = 0;  // chunks of this CTA
+        for (int j = blockIdx.x; j < nitems; j += gridDim.x)
+            if (item_at(p, j, splits, it)) total += it.nchunks;
+        auto blo_chunk = [&](int c) {
+            const int s = c % kStages;
+            mbar_wait(&tfull[s], (c / kStages) & 1);
+            char* st = smem + s * kStageBytes;
+            const float4* hi4 = reinterpret_cast<const float4*>(st);
+            float4* lo4 = reinterpret_cast<float4*>(st + kBBytes);
 #pragma unroll
-            for (int co = 0; co < 64; ++co) out[(long long)co * Part<2>::Ld] = sum[co];
+            for (int u = bt; u < kBBytes / 16; u += kBloThreads) {
+#ifdef WG2_DBG_NO_BLO  // profiling variant: B lo not computed
+                break;
+#endif
+                const float4 b = hi4[u];
+                lo4[u] = make_float4(lo_of(b.x), lo_of(b.y), lo_of(b.z), lo_of(b.w));
+            }
+            asm volatile("fence.proxy.async.shared::cta;");  // B lo -> the MMA's async proxy
+            mbar_arrive(&bready[s]);
+        };
+        if (blo_role && total > 0) blo_chunk(0);
+        int gg = 0, sg = 0;
+        for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
+            if (!item_at(p, j, splits, it)) continue;
+            float sum[64];
+            for (int g = 0; g < it.nchunks; ++g, ++gg) {
+                if (blo_role && gg + 1 < total) blo_chunk(gg + 1);
+                if (g % kSeg != kSeg - 1 && g != it.nchunks - 1) continue;
+                const bool first = g < kSeg;
+                mbar_wait(&accf[t], sg & 1);
+                ++sg;
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t r[32];
+                    tmem_ld16(tacc + 32 * h, r);
+                    tmem_ld16(tacc + 32 * h + 16, r + 16);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;");
+                    if (h == 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        mbar_arrive(&acce[t]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        sum[32 * h + c] = first ? __uint_as_float(r[c]) : __fadd_rn(sum[32 * h + c], __uint_as_float(r[c]));
+                }
+            }
+            if (m < Part<2>::Rows) {
+                float* out = p.act + p.al.stride * it.slot + p.al.p2 + (long long)it.split * G::Co * Part<2>::Ld + m;
+#pragma unroll
+                for (int co = 0; co < 64; ++co) out[(long long)co * Part<2>::Ld] = sum[co];
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");

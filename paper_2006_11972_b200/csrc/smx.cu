@@ -52,6 +52,7 @@ constexpr int kEvalChunk = 16;  // slots evaluated per eval launch group
 struct smx_ctx {
     smx_model_desc d{};
     int device = 0;
+    int num_sms = 148;  // SMs of the device (persistent kernels)
     int S = 0, C = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // second branch of the lockstep (weight gradients)
@@ -319,7 +320,9 @@ void wgrad2_at(smx_ctx* c, const cnn::ConvArgs& a, int splits, int groups) {
            "wgrad2_at smem attribute");
         configured |= bit;
     }
-    cnn::wg2::wgrad2_at_kernel<<<dim3(splits, 1, groups), cnn::wg2::kThreads, cnn::wg2::kSmem, c->cur>>>(a);
+    const int items = splits * groups;
+    cnn::wg2::wgrad2_at_kernel<<<std::min(items, c->num_sms), cnn::wg2::kThreads, cnn::wg2::kSmem, c->cur>>>(
+        a, splits, items);
     launch_check(c, "wgrad2_at");
 }
 
@@ -753,6 +756,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         auto* c = new smx_ctx();
         c->d = d;
         c->device = device;
+        ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
         c->S = n_slots;
         c->C = n_ckpts;
         c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 13 : 14;  // MLP (TC: K5 fused)
