@@ -14,7 +14,7 @@
 //     TMA warp   one 4-D box of the chunk's input window (5 input rows x 33 columns (-1..31) x
 //                32 channels, zero fill = the convolution's padding; 21 KB) + the d2 tile (two
 //                32 x 32 MN-major 128B/32B-atom swizzled boxes, 8 KB) into the stage
-//     producers  (warps 0-3, warp q = TMEM lane quadrant q): for each M tile t the im2col rows of tap 4t + q (lane =
+//     producers  (warps 0-3, warp q = TMEM lane quadrant q; tile 2 by warps 12 / 13): for each M tile t the im2col rows of tap 4t + q (lane =
 //                input channel) straight from the window (input (2r + kh, 2ow + kw) for pixel
 //                (r, ow): one conflict-free LDS per k), split hi / lo, tcgen05.st to a TMEM A slot
 //                (5-slot ring; tile 2 quadrant 1 lane 0 = the all-ones bias row)
@@ -80,6 +80,47 @@ __device__ __forceinline__ bool item_at(const ConvArgs& p, int j, int splits, It
     return it.nchunks > 0;
 }
 
+// One warp's 32 rows of an A slot: tap < 9 -> the tap's im2col rows (lane = input channel) read
+// from the chunk's window, split hi / lo; tap == 9 -> the all-ones bias row (lane 0) and zeros.
+__device__ __forceinline__ void build_rows(int tap, uint32_t ta, const float* win, int lane) {
+    if (tap < 9) {
+        const float* src = win + ((tap / 3) * kWinCols + tap % 3) * G::Ci + lane;
+        float x[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+#ifdef WG2_DBG_NO_WIN  // profiling variant: no window reads
+            x[k] = __int_as_float(0x3f000000 + lane + k);
+#else
+            x[k] = src[((k >> 4) * 2 * kWinCols + 2 * (k & 15)) * G::Ci];
+#endif
+        }
+        tmem_st16(ta, x);
+        tmem_st16(ta + 16, x + 16);
+        float lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) lo[k] = lo_of(x[k]);
+        tmem_st16(ta + 32, lo);
+        tmem_st16(ta + 48, lo + 16);
+    } else {
+        float x[16], z[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            x[k] = lane == 0 ? 1.0f : 0.0f;
+            z[k] = 0.0f;
+        }
+        tmem_st16(ta, x);
+        tmem_st16(ta + 16, x);
+        tmem_st16(ta + 32, z);
+        tmem_st16(ta + 48, z);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+}
+
+__device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0], 2;\n\t}" ::"r"(smem_u32(bar)));
+}
+
 __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p, int splits, int nitems) {
     extern __shared__ __align__(1024) char smem[];
     uint64_t* tfull = reinterpret_cast<uint64_t*>(smem + kBarOff);  // stage landed (TMA tx)
@@ -131,44 +172,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p, int 
                 mbar_wait(&tfull[s], (gg / kStages) & 1);
                 char* st = smem + s * kStageBytes;
                 const float* win = reinterpret_cast<const float*>(st + 2 * kBBytes);
+                // tiles 0 / 1 (taps q, 4 + q); tile 2 (tap 8, the bias row) is built by warps 12 / 13
 #pragma unroll 1
-                for (int t = 0; t < 3; ++t) {
+                for (int t = 0; t < 2; ++t) {
                     const int i = 3 * gg + t, a = i % kASlots;
                     if (i >= kASlots) mbar_wait(&aempty[a], ((i / kASlots) - 1) & 1);
-                    const int tap = 4 * t + q;
-                    const uint32_t ta = tq + kABase + a * 64;
-                    if (tap < 9) {
-                        const float* src = win + ((tap / 3) * kWinCols + tap % 3) * G::Ci + lane;
-                        float x[32];
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) {
-#ifdef WG2_DBG_NO_WIN  // profiling variant: no window reads
-                            x[k] = __int_as_float(0x3f000000 + lane + k);
-#else
-                            x[k] = src[((k >> 4) * 2 * kWinCols + 2 * (k & 15)) * G::Ci];
-#endif
-                        }
-                        tmem_st16(ta, x);
-                        tmem_st16(ta + 16, x + 16);
-                        float lo[32];
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) lo[k] = lo_of(x[k]);
-                        tmem_st16(ta + 32, lo);
-                        tmem_st16(ta + 48, lo + 16);
-                    } else if (tap == 9) {  // tile 2, quadrant 1: row 288 = the all-ones bias row
-                        float x[16], z[16];
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            x[k] = lane == 0 ? 1.0f : 0.0f;
-                            z[k] = 0.0f;
-                        }
-                        tmem_st16(ta, x);
-                        tmem_st16(ta + 16, x);
-                        tmem_st16(ta + 32, z);
-                        tmem_st16(ta + 48, z);
-                    }  // quadrants 2, 3 of tile 2: padding rows, never stored
-                    asm volatile("tcgen05.wait::st.sync.aligned;");
-                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    build_rows(4 * t + q, tq + kABase + a * 64, win, lane);
                     mbar_arrive(&afull[a]);
                 }
             }
@@ -276,6 +285,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p, int 
             float sum[64];
             for (int g = 0; g < it.nchunks; ++g, ++gg) {
                 if (blo_role && gg + 1 < total) blo_chunk(gg + 1);
+                if (t == 2) {  // tile 2's rows: tap 8 (quadrant 0), the bias row (quadrant 1)
+                    const int s = gg % kStages, i = 3 * gg + 2, a = i % kASlots;
+                    mbar_wait(&tfull[s], (gg / kStages) & 1);
+                    if (i >= kASlots) mbar_wait(&aempty[a], ((i / kASlots) - 1) & 1);
+                    build_rows(8 + q, tmem + ((uint32_t)(q * 32) << 16) + kABase + a * 64,
+                               reinterpret_cast<const float*>(smem + s * kStageBytes + 2 * kBBytes), lane);
+                    mbar_arrive2(&afull[a]);  // 64 threads x 2 = the slot's 128 arrivals
+                }
                 if (g % kSeg != kSeg - 1 && g != it.nchunks - 1) continue;
                 const bool first = g < kSeg;
                 mbar_wait(&accf[t], sg & 1);
