@@ -117,6 +117,42 @@ __device__ __forceinline__ void build_rows(int tap, uint32_t ta, const float* wi
     asm volatile("tcgen05.fence::before_thread_sync;");
 }
 
+// The 12 MMAs of one (tile, chunk): 4 k-steps x (A_lo B_hi, A_hi B_lo, A_hi B_hi), one elect and
+// all operand arithmetic inside one asm block (A: +8 TMEM columns, B: +1 KB = 64 descriptor units
+// per k-step), so the issuing warp spends few instructions per MMA.
+__device__ __forceinline__ void mma12(uint32_t d, uint32_t ahi, uint64_t bh, uint64_t bl, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b32 al, ah;\n\t.reg .b64 h, l;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "add.u32 al, %1, 32;\n\tmov.b32 ah, %1;\n\tmov.b64 h, %2;\n\tmov.b64 l, %3;\n\t"
+#ifndef WG2_DBG_NO_LO
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], h, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], l, %4, t;\n\t"
+#else
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], l, %4, p;\n\t"
+#endif
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], h, %4, t;\n\t"
+        "add.u32 al, al, 8;\n\tadd.u32 ah, ah, 8;\n\tadd.u64 h, h, 64;\n\tadd.u64 l, l, 64;\n\t"
+#ifndef WG2_DBG_NO_LO
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], h, %4, t;\n\t"
+#endif
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], l, %4, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], h, %4, t;\n\t"
+        "add.u32 al, al, 8;\n\tadd.u32 ah, ah, 8;\n\tadd.u64 h, h, 64;\n\tadd.u64 l, l, 64;\n\t"
+#ifndef WG2_DBG_NO_LO
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], h, %4, t;\n\t"
+#endif
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], l, %4, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], h, %4, t;\n\t"
+        "add.u32 al, al, 8;\n\tadd.u32 ah, ah, 8;\n\tadd.u64 h, h, 64;\n\tadd.u64 l, l, 64;\n\t"
+#ifndef WG2_DBG_NO_LO
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], h, %4, t;\n\t"
+#endif
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], l, %4, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], h, %4, t;\n\t"
+        "}\n" ::"r"(d), "r"(ahi), "l"(bh), "l"(bl), "r"(idesc), "r"(acc0));
+}
+
 __device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0], 2;\n\t}" ::"r"(smem_u32(bar)));
 }
@@ -224,22 +260,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad2_at_kernel(ConvArgs p, int 
                 const bool seg_start = g % kSeg == 0, seg_end = g % kSeg == kSeg - 1 || g == it.nchunks - 1;
                 const uint32_t bhi = smem_u32(smem + s * kStageBytes), blo = bhi + kBBytes;
                 const uint64_t dbh0 = smem_desc_mn32(bhi, 4096, 512), dbl0 = smem_desc_mn32(blo, 4096, 512);
-                constexpr uint64_t kStep = 1024 >> 4;  // a k-step of 8 MN-major rows
                 for (int t = 0; t < 3; ++t) {
                     const int i = 3 * gg + t, a = i % kASlots;
                     if (seg_start && sg > 0) mbar_wait(&acce[t], (sg - 1) & 1);
                     if (t == 0) mbar_wait(&bready[s], (gg / kStages) & 1);
                     mbar_wait(&afull[a], (i / kASlots) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t dacc = tmem + t * kAccCols, ahi = tmem + kABase + a * 64, alo = ahi + 32;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-#ifndef WG2_DBG_NO_LO  // profiling variant: 2 MMAs per k-step
-                        mma_ts_e(dacc, alo + 8 * k, dbh0 + k * kStep, idesc, (seg_start && k == 0) ? 0u : 1u);
-#endif
-                        mma_ts_e(dacc, ahi + 8 * k, dbl0 + k * kStep, idesc, 1u);
-                        mma_ts_e(dacc, ahi + 8 * k, dbh0 + k * kStep, idesc, 1u);
-                    }
+                    const uint32_t dacc = tmem + t * kAccCols, ahi = tmem + kABase + a * 64;
+                    mma12(dacc, ahi, dbh0, dbl0, idesc, seg_start ? 0u : 1u);
                     mma_commit_e(&aempty[a]);
                     if (seg_end) mma_commit_e(&accf[t]);
                 }
