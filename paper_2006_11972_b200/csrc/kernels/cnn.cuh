@@ -596,6 +596,27 @@ struct Dgrad {
     static constexpr bool kInMaskBits = false, kMaskFromBits = true, kSgd = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
+    // Column position -> parity class.  conv2 orders its 4 classes 0, 1, 3, 2 so that the classes
+    // fed by each output neighbour (da, db) -- those with (pi or !da) and (pj or !db) -- are
+    // contiguous: (0,0) all, (0,1) {1, 3}, (1,0) {3, 2}, (1,1) {3}; the MMAs of a K chunk then
+    // cover only those columns (conv_ws ColRanges): 9 of the 16 class x neighbour blocks are issued.
+    static constexpr bool kColRanges = true;
+    static __host__ __device__ constexpr int cls_at(int pos) { return (L == 2 && pos >= 2) ? (pos ^ 1) : pos; }
+    __device__ __forceinline__ void chunk_cols(int k0, int& off, int& n) const {
+        const int nb = k0 / G::Co, da = nb >> 1, db = nb & 1;
+        constexpr int P = WImg<L>::DgrNTile / G::Ci;  // class positions per N tile
+        int lo = P, hi = -1;
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) {
+            const int cls = cls_at(col0 / G::Ci + pp), pi = cls >> 1, pj = cls & 1;
+            if ((pi || !da) && (pj || !db)) {
+                lo = min(lo, pp);
+                hi = pp;
+            }
+        }
+        off = lo * G::Ci;
+        n = (hi - lo + 1) * G::Ci;
+    }
     const CUtensorMap* tmap;
     const float* dy;
     const float* w;
@@ -658,7 +679,7 @@ struct Dgrad {
     }
     // epilogue column c (0..N-1) -> (class, ci); rows write 4 input pixels
     __device__ __forceinline__ long long pix_off(int r, int col) const {
-        const int cc = col0 + col, cls = cc / G::Ci;
+        const int cc = col0 + col, cls = cls_at(cc / G::Ci);
         const int n = r / (HH * HH), q = r % (HH * HH);
         const int ih = 2 * (q / HH) + (cls >> 1), iw = 2 * (q % HH) + (cls & 1);
         return (((long long)n * G::H + ih) * G::H + iw) * G::Ci + cc % G::Ci;
@@ -811,7 +832,7 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
             const int rem = uu % (WImg<L>::DgrChunks * 8 * NT);
             const int c = rem / (8 * NT), kq = (rem / NT) % 8, r = rem % NT;
             nt = NT;
-            const int cc = half * NT + r, cls = cc / G::Ci, ci = cc % G::Ci;
+            const int cc = half * NT + r, cls = ctc::Dgrad<(L >= 2 ? L : 2)>::cls_at(cc / G::Ci), ci = cc % G::Ci;
             const int pi = cls >> 1, pj = cls & 1;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {

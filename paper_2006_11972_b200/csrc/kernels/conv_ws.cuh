@@ -24,6 +24,8 @@
 // and grouping-invariant like every executor kernel.
 #pragma once
 
+#include <type_traits>
+
 #include "cnn.cuh"
 
 namespace smx {
@@ -81,6 +83,20 @@ constexpr int ws_smem() {
     return WsPlan<Op>::Bytes;
 }
 constexpr int kWsTmemCols = 512;
+
+// Ops whose B tiles have all-zero row blocks for some K chunks (the sub-pixel input gradients: 7 of
+// the 16 (parity class, output neighbour) blocks hold no tap) declare kColRanges and
+// chunk_cols(k0, off, n): the chunk's MMAs then cover only accumulator columns [off, off + n)
+// (a narrower N); the first chunk of every accumulation segment covers all the segment's columns,
+// and the epilogue adds only those.
+template <class Op, class = void>
+struct ColRanges {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct ColRanges<Op, std::void_t<decltype(Op::kColRanges)>> {
+    static constexpr bool value = Op::kColRanges;
+};
 constexpr int kAcc = 128;                        // columns per accumulator
 constexpr int kABase = 256;
 
@@ -562,12 +578,18 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
                     const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
                     const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
+                    // accumulator columns of this chunk (all of them unless the Op skips zero blocks)
+                    int coff = 0, cn = nt;
+                    if constexpr (ColRanges<Op>::value) op.chunk_cols(op.kbeg + c * kKC, coff, cn);
+                    const uint32_t idc = ColRanges<Op>::value ? idesc_tf32(cn) | (Op::B_TMA ? (1u << 16) : 0u) : idesc;
+                    const uint32_t dac = dacc + coff;
                     // descriptors built once per chunk; a k-step of 8 tf32 advances the B tiles by
                     // 2 LBO (the 14-bit address field cannot overflow below 256 KB of smem)
                     // (TMA B: MN-major SWIZZLE_128B_BASE32B -- LBO = 4 KB between 32-column atoms,
                     // SBO = 512 B between 4-row k groups; a k-step of 8 rows advances 1 KB)
-                    const uint64_t dbh0 = Op::B_TMA ? smem_desc_mn32(bhi, 4096, 512) : smem_desc(bhi, lbo, 128);
-                    const uint64_t dbl0 = Op::B_TMA ? smem_desc_mn32(blo, 4096, 512) : smem_desc(blo, lbo, 128);
+                    // (a column range starts coff rows into the K-major B tile: + coff x 16 bytes)
+                    const uint64_t dbh0 = (Op::B_TMA ? smem_desc_mn32(bhi, 4096, 512) : smem_desc(bhi, lbo, 128)) + coff;
+                    const uint64_t dbl0 = (Op::B_TMA ? smem_desc_mn32(blo, 4096, 512) : smem_desc(blo, lbo, 128)) + coff;
                     const uint64_t dstep = Op::B_TMA ? (uint64_t)(1024 >> 4) : (uint64_t)((2 * lbo) >> 4);
 #ifndef SMX_DBG_NO_MMA
                     if (ksteps == 4) {
@@ -575,10 +597,10 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         for (int st = 0; st < 4; ++st) {
                             const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
                             const uint32_t a_off = st * 8;
-                            if (!Op::A_EXACT) mma_ts_e(dacc, alo + a_off, dbh, idesc, (unit_start && st == 0) ? 0u : 1u);
+                            if (!Op::A_EXACT) mma_ts_e(dac, alo + a_off, dbh, idc, (unit_start && st == 0) ? 0u : 1u);
                             if (!Op::B_EXACT)
-                                mma_ts_e(dacc, ahi + a_off, dbl, idesc, (unit_start && st == 0 && Op::A_EXACT) ? 0u : 1u);
-                            mma_ts_e(dacc, ahi + a_off, dbh, idesc,
+                                mma_ts_e(dac, ahi + a_off, dbl, idc, (unit_start && st == 0 && Op::A_EXACT) ? 0u : 1u);
+                            mma_ts_e(dac, ahi + a_off, dbh, idc,
                                    (unit_start && st == 0 && Op::A_EXACT && Op::B_EXACT) ? 0u : 1u);
                         }
                     } else {
@@ -586,14 +608,14 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                             const uint64_t dbh = dbh0 + st * dstep, dbl = dbl0 + st * dstep;
                             uint32_t accum = (unit_start && st == 0) ? 0u : 1u;
                             if (!Op::A_EXACT) {
-                                mma_ts_e(dacc, alo + st * 8, dbh, idesc, accum);
+                                mma_ts_e(dac, alo + st * 8, dbh, idc, accum);
                                 accum = 1u;
                             }
                             if (!Op::B_EXACT) {
-                                mma_ts_e(dacc, ahi + st * 8, dbl, idesc, accum);
+                                mma_ts_e(dac, ahi + st * 8, dbl, idc, accum);
                                 accum = 1u;
                             }
-                            mma_ts_e(dacc, ahi + st * 8, dbh, idesc, accum);
+                            mma_ts_e(dac, ahi + st * 8, dbh, idc, accum);
                         }
                     }
 #endif
@@ -623,6 +645,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         constexpr int kCW = Plan::EpiWarps == 8 ? Plan::N / 2 : Plan::N;  // most columns a warp drains
         // (register sums only where the register budget allows: the 13-warp kernels)
         constexpr bool kRegSum = Plan::EpiWarps == 4 && kCW <= 64 && kCW % 16 == 0;
+        static_assert(!(kRegSum && ColRanges<Op>::value), "column ranges need the shared-memory segment sums");
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
@@ -711,17 +734,28 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         asm volatile("tcgen05.fence::before_thread_sync;");
                         mbar_arrive(&acce[acc_i]);
                     }
+                    // columns written in this segment (Ops skipping zero blocks: the first chunk's range)
+                    int slo = 0, shi = nt;
+                    if constexpr (ColRanges<Op>::value) {
+                        int sn;
+                        op.chunk_cols(op.kbeg + j * seg * kKC, slo, sn);
+                        shi = slo + sn;
+                    }
                     // 32 columns per TMEM round trip (two loads in flight before one wait)
                     for (int c0 = cbeg; c0 < cbeg + cw; c0 += 32) {
                         uint32_t r[32];
                         const bool two = c0 + 16 < cbeg + cw;
-                        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
-                        if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0 + 16, r + 16);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;");
+                        const bool use = !ColRanges<Op>::value || (c0 < shi && c0 + 32 > slo);
+                        if (use) {
+                            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0, r);
+                            if (two) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0 + 16, r + 16);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;");
+                        }
                         if (c0 + 32 >= cbeg + cw) {
                             asm volatile("tcgen05.fence::before_thread_sync;");
                             mbar_arrive(&acce[acc_i]);
                         }
+                        if (!use) continue;
 #pragma unroll
                         for (int jj = 0; jj < 32; jj += 4) {
                             if (jj >= 16 && !two) break;
