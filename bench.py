@@ -33,13 +33,28 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-# DRAM bytes (read + write) per launch of the roofline kernel from one `ncu --set full` capture
-# (profiles/<round>/), keyed by kernel; filled in after each capture.
+# DRAM bytes (read + write) per launch of each candidate roofline kernel (64 groups at bs 128)
+# from one `ncu --set full` capture of a 64-slot lockstep (profiles/r02/ncu_convs_v14.txt)
 TRAFFIC: dict = {
-    # profiles/r01/ncu_conv2_fwd_full.txt: 64 groups at bs 128 (= the bench's roofline launch)
-    "conv_ws_kernel<Fwd<2>>": 1_083_516_000 + 506_999_552,
-    # profiles/r01/ncu_wgrad2_full.txt: conv2 weight-gradient GEMM, 64 groups at bs 128
-    "conv_ws_kernel<Wgrad<2>>": 1_674_893_000 + 75_405_000,
+    "K1_conv2_fwd": 1_083_998_000 + 539_703_000,
+    "K3_conv2_wgrad": 1_613_875_000 + 70_186_000,
+    "K2_conv2_dgrad": 587_868_000 + 1_017_241_000,
+    "K2_conv3_dgrad": 349_032_000 + 487_305_000,
+    "K1_conv3_fwd": 576_542_000 + 254_631_000,
+    "K3_conv3_wgrad": 838_719_000 + 71_447_000,
+}
+# what each candidate is (tensor-core mode, per launch = 64 groups at bs 128)
+KERNEL_DESC: dict = {
+    "K1_conv2_fwd": "conv_ws_kernel<Fwd<2>> (conv2 forward implicit GEMM, 64 groups x M 32768 x N 64 x K 288)",
+    "K3_conv2_wgrad": "wgrad2_at_kernel (conv2 weight gradient, all 9 taps per persistent CTA, 64 groups x M 289 "
+                      "x N 64 x K 32768 in 16 splits)",
+    "K2_conv2_dgrad": "conv_ws_kernel<Dgrad<2>> (conv2 input gradient, sub-pixel GEMM, 64 groups x M 8192 x N 128 "
+                      "x K 256, 9 of 16 class x neighbour blocks issued)",
+    "K2_conv3_dgrad": "conv_ws_kernel<Dgrad<3>> (conv3 input gradient, sub-pixel GEMM, 64 groups x M 2048 x N 2x128 "
+                      "x K 256/512)",
+    "K1_conv3_fwd": "conv_ws_kernel<Fwd<3>> (conv3 forward implicit GEMM, 64 groups x M 8192 x N 128 x K 576)",
+    "K3_conv3_wgrad": "conv_ws_kernel<Wgrad<3>> + wgrad_reduce<3> (conv3 weight gradient, 64 groups x M 577 x N 128 "
+                      "x K 8192, + the split reduction with the fused SGD update)",
 }
 METRIC = "trial-equivalent train steps/sec per study"
 UNIT = "trial-steps/s"
@@ -441,11 +456,12 @@ def main():
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
-        # the largest kernel share of the bench (profiles/r01/launches_bench_c2_mid.txt): the conv2
-        # weight gradient, M 288 (tap, cin) x N 64 (cout) x K 32768 (sample, pixel) per group
-        roofline = dict(kernels["K3_conv2_wgrad"])
-        roofline["kernel"] = ("conv_ws_kernel<Wgrad<2>> (conv2 weight-gradient implicit GEMM, 64 groups x M 288 x "
-                              "N 64 x K 32768, split 16 ways)" if gemm_mode == ex.GEMM_TC else "conv_wgrad_simt<2>")
+        # the roofline kernel is the dominant one: the longest of the six implicit GEMMs (each has the
+        # same algorithmic product count per launch), i.e. the largest share of the lockstep
+        dom = max(KERNEL_DESC, key=lambda k: kernels[k]["ms_per_launch"]) if gemm_mode == ex.GEMM_TC else "K3_conv2_wgrad"
+        roofline = dict(kernels[dom])
+        roofline["kernel"] = KERNEL_DESC[dom] if gemm_mode == ex.GEMM_TC else "conv_wgrad_simt<2>"
+        roofline["traffic"] = TRAFFIC.get(dom) if gemm_mode == ex.GEMM_TC else None
     else:
         kernels = {
             "K1_fwd1_gemm": tensor("fwd1", gemm_flops, ms[2]),
@@ -455,7 +471,7 @@ def main():
         }
         roofline = dict(kernels["K1_fwd1_gemm"])
         roofline["kernel"] = "conv_ws_kernel<DenseOp<0,0,BiasRelu,exact A>> (MLP layer-1 forward, 64 groups x 128x256x784)"
-    roofline["traffic"] = TRAFFIC.get(roofline["kernel"].split(" ")[0])
+        roofline["traffic"] = None
 
     # ---- K7: checkpoint fork to another GPU (smx_ckpt_peer_copy, NVLink P2P); on a 1-GPU box the
     # same call between two contexts of the one device (a device-local copy), labelled as such
