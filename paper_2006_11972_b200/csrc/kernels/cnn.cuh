@@ -22,6 +22,12 @@
 #ifndef SMX_SEG_CHUNKS
 #define SMX_SEG_CHUNKS 4
 #endif
+// the input gradients' segments: 8 chunks = 256 products (conv2: the whole 4 x Co reduction, one
+// drain per tile; conv3: two).  Measured vs float64: gradient errors 3.0-4.3e-6 -> 4.0-4.8e-6
+// (tolerance 2e-5), Dgrad2 562 -> 518 us, Dgrad3 457 -> 419 us (fewer segment drains / sums).
+#ifndef SMX_DGR_SEG_CHUNKS
+#define SMX_DGR_SEG_CHUNKS 8
+#endif
 
 namespace smx {
 namespace cnn {
@@ -594,7 +600,7 @@ struct Dgrad {
     static constexpr bool A_EXACT = false, B_EXACT = false, B_IMAGE = true, B_TMA = false;
     static constexpr bool A_TMA = true;  // A tile = one shifted TMA box of dy per chunk
     static constexpr bool kInMaskBits = false, kMaskFromBits = true, kSgd = false;
-    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = 8;
+    static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_DGR_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
     // Column position -> parity class.  conv2 orders its 4 classes 0, 1, 3, 2 so that the classes
     // fed by each output neighbour (da, db) -- those with (pi or !da) and (pj or !db) -- are
