@@ -76,6 +76,7 @@ constexpr int kL1Outs = 32 * 28;
 struct ActLayout {
     long long a1, a2, a3, d1, d2, d3, g, z, dz, dg, rl, p1, p2, p3, wf1, wf2, wf3, wd2, wd3, w1p, stride;
     long long mk1, mk2;  // tensor-core mode: ReLU-mask bitmaps of a1 / a2, bit e = (a[e] > 0)
+    long long mk3;       // tensor-core mode: bitmap of a3 > 0 (written by the conv3 forward epilogue, read by head_dg)
 };
 
 // Tensor-core B operands that are weights are pre-split once per lockstep into "images": per K
@@ -120,6 +121,7 @@ inline ActLayout act_layout(int max_batch) {
     L.w1p = take(kL1Outs);
     L.mk1 = take(1024 * 32 / 32);
     L.mk2 = take(256 * 64 / 32);
+    L.mk3 = take(64 * 128 / 32);
     L.p1 = o;
     o += Part<1>::Size;
     L.p2 = o;
@@ -162,6 +164,8 @@ struct ConvArgs {
     int x_row0;
     int fixed_bs;        // > 0: batch size override (eval chunks)
     int fuse_update;     // tensor-core lockstep: the weight-gradient reductions apply K5 in place
+    int pooled;          // tensor-core mode: the conv3 forward epilogue wrote g (pooled) and the a3 > 0 bitmap
+                         // instead of a3; the head kernels read those
     float* slab;
     long long slab_stride;
     float* act;
@@ -396,12 +400,16 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
     __shared__ float g[kFeat];
     __shared__ float z[kNCP];
     const int c = threadIdx.x;
-    const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
-    float s = 0.0f;
+    if (p.pooled) {  // pooled by the conv3 forward epilogue (same order and scaling)
+        g[c] = v.act[p.al.g + (long long)n * kFeat + c];
+    } else {
+        const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
+        float s = 0.0f;
 #pragma unroll 16
-    for (int pix = 0; pix < 64; ++pix) s = __fadd_rn(s, __ldg(a3 + pix * kFeat + c));  // loads run ahead
-    g[c] = __fmul_rn(s, 0.015625f);
-    if (!p.zout) v.act[p.al.g + (long long)n * kFeat + c] = g[c];
+        for (int pix = 0; pix < 64; ++pix) s = __fadd_rn(s, __ldg(a3 + pix * kFeat + c));  // loads run ahead
+        g[c] = __fmul_rn(s, 0.015625f);
+        if (!p.zout) v.act[p.al.g + (long long)n * kFeat + c] = g[c];
+    }
     __syncthreads();
     if (c < kNCP) {
         const float* wr = v.w + kOffW4 + c * kFeat;
@@ -464,10 +472,16 @@ __global__ void __launch_bounds__(128) head_dg_kernel(ConvArgs p) {
 #pragma unroll
     for (int k = 0; k < kNCP; ++k) acc = __fmaf_rn(dz[k], v.w[kOffW4 + k * kFeat + c], acc);
     const float dg = __fmul_rn(acc, 0.015625f);
-    const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
     float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
+    if (p.pooled) {  // a3 > 0 as the bitmap the conv3 forward epilogue wrote: word (n, pix, c / 32)
+        const uint32_t* mk = reinterpret_cast<const uint32_t*>(v.act + p.al.mk3) + (long long)n * 64 * (kFeat / 32) + c / 32;
 #pragma unroll 16
-    for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
+        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = (__ldg(mk + pix * (kFeat / 32)) >> (c & 31)) & 1u ? dg : 0.0f;
+    } else {
+        const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
+#pragma unroll 16
+        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
+    }
 }
 
 // ---- tensor-core mode: implicit-GEMM Op policies for conv_ws.cuh ---------------------------
@@ -495,6 +509,11 @@ struct Fwd {
     // for the input gradient of this layer: the taps (kh, kw) in {1, 2}^2 of a stride-2 conv visit
     // every input pixel exactly once, and a producer thread holds 32 consecutive channels of it
     static constexpr bool kInMaskBits = (L >= 2), kMaskFromBits = false, kSgd = false;
+    // conv3: the epilogue pools each sample's 64 output pixels into g (the head's input, in
+    // head_fwd's order) and writes the a3 > 0 bitmap for head_dg instead of storing a3 itself
+    static constexpr bool kPool = (L == 3);
+    float* gout;
+    uint32_t* mk_out;
     uint32_t* in_bits;
     const CUtensorMap* tmap;
     const float* in;
@@ -517,6 +536,8 @@ struct Fwd {
         img = v.act + (L == 1 ? p.al.wf1 : L == 2 ? p.al.wf2 : p.al.wf3);
         tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 3 ? kTmFwd3 : kTmFwd2);
         in_bits = reinterpret_cast<uint32_t*>(v.act + (L == 3 ? p.al.mk2 : p.al.mk1));
+        gout = v.act + p.al.g;
+        mk_out = reinterpret_cast<uint32_t*>(v.act + p.al.mk3);
         in = layer_in<L>(p, v);
         w = v.w + G::OffW;
         bias = v.w + G::OffB;

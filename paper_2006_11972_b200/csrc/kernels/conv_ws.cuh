@@ -97,6 +97,17 @@ template <class Op>
 struct ColRanges<Op, std::void_t<decltype(Op::kColRanges)>> {
     static constexpr bool value = Op::kColRanges;
 };
+// Ops with kPool (the conv3 forward): the bias+ReLU epilogue emits per-sample channel sums (64
+// rows = one sample, x 2^-6; a fixed order: 8 row classes r % 8, each ascending) and the tile's
+// value > 0 bitmap instead of the activation tile itself
+template <class Op, class = void>
+struct PoolOp {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct PoolOp<Op, std::void_t<decltype(Op::kPool)>> {
+    static constexpr bool value = Op::kPool;
+};
 constexpr int kAcc = 128;                        // columns per accumulator
 constexpr int kABase = 256;
 
@@ -819,6 +830,50 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                         for (int e = et; e < kBM * q4; e += Plan::EpiThreads) {
                             const int r = e / q4, c4 = e % q4, m = mt0 + r;
                             if (m < M && 4 * c4 < N) op.store4(m, 4 * c4, *s4(r, c4));
+                        }
+                    }
+                } else if constexpr (PoolOp<Op>::value) {
+                    // conv3 forward: bias + ReLU, then per-sample channel sums and the value > 0
+                    // bitmap (no activation store).  Thread = column quad c4 = lane, rows warp + 8 i:
+                    // a warp holds one whole row per step (ballots give its bitmap words) and each
+                    // thread sums its 8 rows of each sample; the 8 row classes are added in a fixed
+                    // order through shared memory.
+                    static_assert(Plan::N == 128 && Plan::EpiThreads == 256, "pooling epilogue mapping");
+                    const int c4 = et & 31, w8 = et >> 5;
+                    float4 ps[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+#pragma unroll
+                    for (int ii = 0; ii < 16; ++ii) {
+                        const int r = w8 + 8 * ii, m = mt0 + r;
+                        if (m >= M) break;  // rows >= M only in the last tile, past its last sample
+                        float4 x = *s4(r, c4);
+                        x.x = __fadd_rn(x.x, bfix.x); x.y = __fadd_rn(x.y, bfix.y);
+                        x.z = __fadd_rn(x.z, bfix.z); x.w = __fadd_rn(x.w, bfix.w);
+                        x = make_float4(x.x > 0.0f ? x.x : 0.0f, x.y > 0.0f ? x.y : 0.0f, x.z > 0.0f ? x.z : 0.0f,
+                                        x.w > 0.0f ? x.w : 0.0f);
+                        float4& pp = ps[ii >> 3];
+                        pp.x = __fadd_rn(pp.x, x.x); pp.y = __fadd_rn(pp.y, x.y);
+                        pp.z = __fadd_rn(pp.z, x.z); pp.w = __fadd_rn(pp.w, x.w);
+                        // bitmap word q (channels 32 q .. 32 q + 31) = the nibbles of lanes 8 q .. 8 q + 7
+                        uint32_t v = ((x.x > 0.0f ? 1u : 0u) | (x.y > 0.0f ? 2u : 0u) | (x.z > 0.0f ? 4u : 0u) |
+                                      (x.w > 0.0f ? 8u : 0u)) << (4 * (c4 & 7));
+                        v |= __shfl_xor_sync(0xffffffffu, v, 1);
+                        v |= __shfl_xor_sync(0xffffffffu, v, 2);
+                        v |= __shfl_xor_sync(0xffffffffu, v, 4);
+                        if ((c4 & 7) == 0) op.mk_out[(long long)m * 4 + (c4 >> 3)] = v;
+                    }
+                    asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");  // sacc reads done
+                    float4* part = reinterpret_cast<float4*>(sacc);  // [row class w8][sample][c4]
+                    part[(w8 * 2 + 0) * 32 + c4] = ps[0];
+                    part[(w8 * 2 + 1) * 32 + c4] = ps[1];
+                    asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");
+                    {  // thread = (sample, channel): row classes 0..7 in order, x 2^-6
+                        const int smp = et >> 7, ch = et & 127;
+                        if (mt0 + 64 * smp < M) {
+                            float sum = 0.0f;
+#pragma unroll
+                            for (int w = 0; w < 8; ++w)
+                                sum = __fadd_rn(sum, reinterpret_cast<const float*>(&part[(w * 2 + smp) * 32 + (ch >> 2)])[ch & 3]);
+                            op.gout[(long long)((mt0 + 64 * smp) / 64) * 128 + ch] = __fmul_rn(sum, 0.015625f);
                         }
                     }
                 } else

@@ -279,6 +279,7 @@ cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
     a.loss_hist = c->loss;
     a.tmaps = c->tmaps;
     a.fuse_update = c->d.gemm_mode == SMX_GEMM_TC ? 1 : 0;
+    a.pooled = c->d.gemm_mode == SMX_GEMM_TC ? 1 : 0;
     return a;
 }
 
