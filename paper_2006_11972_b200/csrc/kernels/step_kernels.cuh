@@ -264,8 +264,17 @@ struct CopyJob {
     SlotState* dst_st;
 };
 
-__global__ void __launch_bounds__(256) fork_copy_kernel(const CopyJob* jobs, long long n4) {
-    const CopyJob j = jobs[blockIdx.y];
+// Jobs travel as a kernel parameter (no job-list H2D, no host sync between forks): one launch
+// moves up to N (slot, entry) pairs, blockIdx.y = job.  N = 16 for the engine's forks (512 B
+// of parameters), 256 for the bench's many-checkpoint K6 measurement.
+template <int N>
+struct CopyBatch {
+    CopyJob j[N];
+};
+
+template <int N>
+__global__ void __launch_bounds__(256) fork_copy_kernel(const __grid_constant__ CopyBatch<N> jobs, long long n4) {
+    const CopyJob j = jobs.j[blockIdx.y];
     const long long stride = (long long)gridDim.x * blockDim.x;
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     // 4 independent 16-byte loads in flight per thread

@@ -58,6 +58,7 @@ struct smx_ctx {
     cudaStream_t side = nullptr;  // second branch of the lockstep (weight gradients)
     cudaStream_t cur = nullptr;   // stream the GEMM / reduction helpers enqueue on
     cudaEvent_t fj[4] = {};       // fork / join events of the lockstep branches
+    cudaEvent_t xev = nullptr;    // cross-context ordering of peer copies (K7)
 
     float* slab = nullptr;      // S x 2 x PAlloc  (w | m)
     float* grad = nullptr;      // S x PAlloc
@@ -75,8 +76,6 @@ struct smx_ctx {
     float* eval_scratch = nullptr;
     double* eval_out = nullptr;
     int* eval_slots = nullptr;
-    CopyJob* jobs = nullptr;    // device job list for fork copies
-    int jobs_cap = 0;
     std::vector<char> ck_valid;
     std::vector<char> slot_live;  // slot holds a state (init / load / write since open or release)
     // every training / validation input value is exact in tf32 (true for the synthetic k/128
@@ -695,17 +694,16 @@ unsigned fork_blocks(long long n4) { return (unsigned)std::max<long long>(1, std
 
 void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
     if (jobs.empty()) return;
-    if ((int)jobs.size() > c->jobs_cap) {
-        if (c->jobs) cudaFree(c->jobs);
-        c->jobs_cap = (int)jobs.size() * 2;
-        ck(cudaMalloc(&c->jobs, sizeof(CopyJob) * c->jobs_cap), "cudaMalloc jobs");
-    }
-    ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * jobs.size(), cudaMemcpyHostToDevice, c->stream),
-       "jobs H2D");
+    constexpr int kB = 16;
     const long long n4 = 2 * c->palloc / 4;
     if (c->timing) cudaEventRecord(c->ev[4], c->stream);
-    fork_copy_kernel<<<dim3(fork_blocks(n4), (unsigned)jobs.size()), 256, 0, c->stream>>>(c->jobs, n4);
-    launch_check(c, "fork_copy");
+    for (std::size_t i0 = 0; i0 < jobs.size(); i0 += kB) {
+        const int nj = (int)std::min<std::size_t>(kB, jobs.size() - i0);
+        CopyBatch<kB> b{};
+        for (int i = 0; i < nj; ++i) b.j[i] = jobs[i0 + i];
+        fork_copy_kernel<kB><<<dim3(fork_blocks(n4), (unsigned)nj), 256, 0, c->stream>>>(b, n4);
+        launch_check(c, "fork_copy");
+    }
     if (c->timing) {
         cudaEventRecord(c->ev[5], c->stream);
         cudaEventSynchronize(c->ev[5]);
@@ -714,8 +712,8 @@ void run_copy(smx_ctx* c, const std::vector<CopyJob>& jobs) {
         c->stats.fork_ms += ms;
         c->stats.fork_launches += 1;
     }
-    // the job list lives in device memory reused by the next copy: keep ordering simple
-    ck(cudaStreamSynchronize(c->stream), "fork sync");
+    // no host sync: the jobs are kernel parameters and every later reader of the slot / entry is
+    // ordered behind the copy on the same stream
     c->stats.forks += (long long)jobs.size();
 }
 
@@ -775,6 +773,7 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
             c->cur = c->stream;
             for (auto& e : c->fj) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "fork event");
+            ck(cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming), "peer event");
             const long long P2 = 2 * c->palloc;
             ck(cudaMalloc(&c->slab, sizeof(float) * P2 * n_slots), "slab");
             ck(cudaMalloc(&c->grad, sizeof(float) * c->palloc * n_slots), "grad");
@@ -824,12 +823,13 @@ int smx_close(smx_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_graphs(c);
     void* bufs[] = {c->slab, c->grad, c->pool, c->st, c->ck_st, c->hp, c->loss, c->act, c->xtrain, c->ytrain,
-                    c->xval, c->yval, c->eval_act, c->zval, c->eval_scratch, c->eval_out, c->eval_slots, c->jobs,
+                    c->xval, c->yval, c->eval_act, c->zval, c->eval_scratch, c->eval_out, c->eval_slots,
                     c->scratch_slots, c->tmaps, c->flag};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->xev) cudaEventDestroy(c->xev);
     for (auto& e : c->fj)
         if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
@@ -1007,8 +1007,13 @@ int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
         check_ckpt(src, src_ckpt);
         if (!src->ck_valid[src_ckpt]) fail(SMX_EINTEGRITY, "peer copy from empty checkpoint entry");
         if (dst->palloc != src->palloc) fail(SMX_ECONFIG, "peer copy between different models");
-        ck(cudaStreamSynchronize(src->stream), "src sync");
+        // the copy runs on the destination stream behind everything the source stream has queued
+        // (the SAVE that filled the entry), and the source stream waits for the copy before it
+        // can overwrite the entry: device-side ordering, no host sync
+        cudaSetDevice(src->device);
+        ck(cudaEventRecord(src->xev, src->stream), "src record");
         cudaSetDevice(dst->device);
+        ck(cudaStreamWaitEvent(dst->stream, src->xev, 0), "dst wait");
         bool direct = dst->device == src->device;
         if (!direct) {
             int can = 0;
@@ -1026,15 +1031,10 @@ int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
             CopyJob j{reinterpret_cast<const float4*>(src->pool + src->slab_stride() * src_ckpt),
                       reinterpret_cast<float4*>(dst->pool + dst->slab_stride() * dst_ckpt), src->ck_st + src_ckpt,
                       dst->ck_st + dst_ckpt};
-            if (!dst->jobs || dst->jobs_cap < 1) {
-                if (dst->jobs) cudaFree(dst->jobs);
-                dst->jobs_cap = 2;
-                ck(cudaMalloc(&dst->jobs, sizeof(CopyJob) * dst->jobs_cap), "cudaMalloc jobs");
-            }
-            ck(cudaMemcpyAsync(dst->jobs, &j, sizeof j, cudaMemcpyHostToDevice, dst->stream), "job H2D");
+            CopyBatch<1> b{{j}};
             const long long n4 = 2 * dst->palloc / 4;
             if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
-            fork_copy_kernel<<<dim3(fork_blocks(n4), 1), 256, 0, dst->stream>>>(dst->jobs, n4);
+            fork_copy_kernel<1><<<dim3(fork_blocks(n4), 1), 256, 0, dst->stream>>>(b, n4);
             launch_check(dst, "peer fork_copy");
         } else {  // no peer access between these GPUs: the runtime's staged peer copy
             if (dst->timing) cudaEventRecord(dst->ev[4], dst->stream);
@@ -1054,7 +1054,10 @@ int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
             dst->stats.fork_ms += ms;
             dst->stats.fork_launches += 1;
         }
-        ck(cudaStreamSynchronize(dst->stream), "peer sync");
+        ck(cudaEventRecord(dst->xev, dst->stream), "dst record");
+        cudaSetDevice(src->device);
+        ck(cudaStreamWaitEvent(src->stream, dst->xev, 0), "src wait");
+        cudaSetDevice(dst->device);
         dst->ck_valid[dst_ckpt] = 1;
         dst->stats.forks += 1;
     });
@@ -1296,20 +1299,15 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             cudaEventRecord(c->ev[7], c->stream);
         } else if (kind == 1) {
             if (n > c->C || n > c->S) fail(SMX_ECONFIG, "more checkpoints than allocated");
-            std::vector<CopyJob> jobs(n);
+            if (n > 256) fail(SMX_ECONFIG, "at most 256 fork jobs per measured launch");
+            CopyBatch<256> jobs{};
             for (int i = 0; i < n; ++i)
-                jobs[i] = CopyJob{reinterpret_cast<const float4*>(c->slab + c->slab_stride() * i),
-                                  reinterpret_cast<float4*>(c->pool + c->slab_stride() * i), c->st + i, c->ck_st + i};
-            if (n > c->jobs_cap) {
-                if (c->jobs) cudaFree(c->jobs);
-                c->jobs_cap = n * 2;
-                ck(cudaMalloc(&c->jobs, sizeof(CopyJob) * c->jobs_cap), "jobs");
-            }
-            ck(cudaMemcpyAsync(c->jobs, jobs.data(), sizeof(CopyJob) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+                jobs.j[i] = CopyJob{reinterpret_cast<const float4*>(c->slab + c->slab_stride() * i),
+                                    reinterpret_cast<float4*>(c->pool + c->slab_stride() * i), c->st + i, c->ck_st + i};
             const long long n4 = 2 * c->palloc / 4;
-            for (int w = 0; w < 3; ++w) fork_copy_kernel<<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(c->jobs, n4);
+            for (int w = 0; w < 3; ++w) fork_copy_kernel<256><<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(jobs, n4);
             cudaEventRecord(c->ev[6], c->stream);
-            for (int r = 0; r < reps; ++r) fork_copy_kernel<<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(c->jobs, n4);
+            for (int r = 0; r < reps; ++r) fork_copy_kernel<256><<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(jobs, n4);
             cudaEventRecord(c->ev[7], c->stream);
         } else if (kind >= 2 && kind <= 7 && c->cnn) {
             if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
