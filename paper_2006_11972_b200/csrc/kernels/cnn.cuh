@@ -148,10 +148,12 @@ inline ActLayout act_layout(int max_batch) {
 // stride of 2), the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients, and
 // the weight gradients' im2col operands (a1 / a2 again, one box of 32 output pixels x all input
 // channels per tap).
-enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmWgB2 = 6, kTmWgB3 = 7, kTmapKinds = 8 };
+enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmWgB2 = 6, kTmWgB3 = 7, kTmA1 = 8, kTmapKinds = 9 };
 // kTmWgB2 / kTmWgB3: the weight gradients' B operand (the layer's output gradient d2 / d3 as a
 // 2-D [sample x pixel][Co] tensor): 32 x 32 boxes with the 128-byte / 32-byte-atom swizzle = the
 // UMMA MN-major tf32 layout (SWIZZLE_128B_BASE32B), loaded straight into the B stage.
+// kTmA1: a1 as a 2-D [sample x pixel][32] tensor, boxes of one image row (32 pixels x 128 B) with
+// the 128-byte swizzle: the conv1 forward's output tiles leave shared memory by TMA stores.
 
 struct ConvArgs {
     const int* slots;
@@ -1095,9 +1097,9 @@ __global__ void __launch_bounds__(256, 2) conv1_wgrad_lane(ConvArgs p) {
     }
 }
 
-// Sum the per-sample partials in sample order into the gradient slab, or (fuse_update) apply K5
-// to the parameter in place.  grid (7, groups), block 128.
-__global__ void __launch_bounds__(128) conv1_wgrad_reduce(ConvArgs p) {
+// Sum the partial rows (one per `per_part` consecutive samples) in order into the gradient slab,
+// or (fuse_update) apply K5 to the parameter in place.  grid (7, groups), block 128.
+__global__ void __launch_bounds__(128) conv1_wgrad_reduce(ConvArgs p, int per_part) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* part = v.act + p.al.w1p;
     float* g = p.grad + p.grad_stride * v.slot;
@@ -1107,7 +1109,7 @@ __global__ void __launch_bounds__(128) conv1_wgrad_reduce(ConvArgs p) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kL1Outs; i += gridDim.x * blockDim.x) {
         float s_ = 0.0f;
 #pragma unroll 8
-        for (int n = 0; n < v.bs; ++n) s_ = __fadd_rn(s_, __ldg(part + (long long)n * kL1Outs + i));
+        for (int n = 0; n < (v.bs + per_part - 1) / per_part; ++n) s_ = __fadd_rn(s_, __ldg(part + (long long)n * kL1Outs + i));
         const int co = i / 28, j = i % 28;
         const long long at = j < 27 ? Geo<1>::OffW + (co * 9 + j / 3) * 4 + j % 3 : Geo<1>::OffB + co;
         if (p.fuse_update)

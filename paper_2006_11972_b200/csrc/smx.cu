@@ -27,6 +27,7 @@
 #include "kernels/conv_ws.cuh"
 #include "kernels/dense_ws.cuh"
 #include "kernels/wgrad2_at.cuh"
+#include "kernels/conv1_tc.cuh"
 
 using namespace smx;
 
@@ -255,6 +256,18 @@ void make_conv_tmaps(smx_ctx* c) {
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (B) failed (" + std::to_string((int)r) + ")");
         }
+    // the conv1 forward's output a1 as [max_batch x 1024 pixels][32], one image row per box
+    for (int s = 0; s < c->S; ++s) {
+        float* base = c->act + c->act_stride * s + c->al.a1;
+        const cuuint64_t dims[2] = {32, (cuuint64_t)(mb * 1024)};
+        const cuuint64_t strides[1] = {32 * 4};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t es[2] = {1, 1};
+        const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + cnn::kTmA1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base,
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (a1) failed (" + std::to_string((int)r) + ")");
+    }
     ck(cudaMalloc(&c->tmaps, sizeof(CUtensorMap) * h.size()), "tensor maps");
     ck(cudaMemcpy(c->tmaps, h.data(), sizeof(CUtensorMap) * h.size(), cudaMemcpyHostToDevice), "tensor maps H2D");
 }
@@ -326,12 +339,61 @@ void wgrad2_at(smx_ctx* c, const cnn::ConvArgs& a, int splits, int groups) {
     launch_check(c, "wgrad2_at");
 }
 
+// conv1 weight gradient on the tensor cores (kernels/conv1_tc.cuh): persistent grid, 2 CTAs per SM,
+// one work item per (slot, group of kImgs samples) -> one partial row each
+void conv1_wgrad_tc(smx_ctx* c, const cnn::ConvArgs& a, int mb, int groups) {
+    namespace c1 = cnn::c1;
+    static unsigned long long configured = 0;
+    const unsigned long long bit = 1ull << (c->device & 63);
+    if (!(configured & bit)) {
+        ck(cudaFuncSetAttribute(c1::conv1_wgrad_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1::kSmem),
+           "conv1_wgrad_tc smem attribute");
+        ck(cudaFuncSetAttribute(c1::conv1_wgrad_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c1::kSmem),
+           "conv1_wgrad_tc smem attribute");
+        configured |= bit;
+    }
+    const int parts = (mb + c1::kImgs - 1) / c1::kImgs, items = parts * groups;
+    const int grid = std::min(items, 2 * c->num_sms);
+    if (c->data_tf32_exact)
+        c1::conv1_wgrad_tc_kernel<true><<<grid, c1::kThreads, c1::kSmem, c->cur>>>(a, parts, items);
+    else
+        c1::conv1_wgrad_tc_kernel<false><<<grid, c1::kThreads, c1::kSmem, c->cur>>>(a, parts, items);
+    launch_check(c, "conv1_wgrad_tc");
+}
+
+// conv1 forward on the tensor cores (kernels/conv1_tc.cuh, namespace f1): 2 CTAs per SM, items
+// (slot, sample) in contiguous per-CTA ranges
+void conv1_fwd_tc(smx_ctx* c, const cnn::ConvArgs& a, int mb, int groups) {
+    namespace f1 = cnn::c1::f1;
+    static unsigned long long configured = 0;
+    const unsigned long long bit = 1ull << (c->device & 63);
+    if (!(configured & bit)) {
+        ck(cudaFuncSetAttribute(f1::conv1_fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f1::kSmem),
+           "conv1_fwd_tc smem attribute");
+        ck(cudaFuncSetAttribute(f1::conv1_fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f1::kSmem),
+           "conv1_fwd_tc smem attribute");
+        configured |= bit;
+    }
+    const int items = mb * groups;
+    const int grid = std::min(items, 2 * c->num_sms);
+    if (c->data_tf32_exact)
+        f1::conv1_fwd_tc_kernel<true><<<grid, f1::kThreads, f1::kSmem, c->cur>>>(a, mb, items);
+    else
+        f1::conv1_fwd_tc_kernel<false><<<grid, f1::kThreads, f1::kSmem, c->cur>>>(a, mb, items);
+    launch_check(c, "conv1_fwd_tc");
+}
+
 template <int L>
 void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        cnn::conv1_fwd_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
-        launch_check(c, "conv1_fwd_lane");
+        static const bool lane_kernel = std::getenv("SMX_CONV1_FWD_LANE") != nullptr;  // A/B: the FFMA2 kernel
+        if (lane_kernel) {
+            cnn::conv1_fwd_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
+            launch_check(c, "conv1_fwd_lane");
+        } else {
+            conv1_fwd_tc(c, a, mb, n);
+        }
         return;
     }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
@@ -347,9 +409,14 @@ template <int L>
 void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        cnn::conv1_wgrad_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
-        launch_check(c, "conv1_wgrad_lane");
-        cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a);
+        static const bool lane_kernel = std::getenv("SMX_CONV1_WGRAD_LANE") != nullptr;  // A/B: the FFMA2 kernel
+        if (lane_kernel) {
+            cnn::conv1_wgrad_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
+            launch_check(c, "conv1_wgrad_lane");
+        } else {
+            conv1_wgrad_tc(c, a, mb, n);
+        }
+        cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a, lane_kernel ? 1 : cnn::c1::kImgs);
         launch_check(c, "conv1_wgrad_reduce");
         return;
     }
@@ -1309,7 +1376,7 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
             cudaEventRecord(c->ev[6], c->stream);
             for (int r = 0; r < reps; ++r) fork_copy_kernel<256><<<dim3(fork_blocks(n4), n), 256, 0, c->stream>>>(jobs, n4);
             cudaEventRecord(c->ev[7], c->stream);
-        } else if (kind >= 2 && kind <= 7 && c->cnn) {
+        } else if (kind >= 2 && kind <= 9 && c->cnn) {
             if (n > c->S) fail(SMX_ECONFIG, "more slots than allocated");
             std::vector<int> v(n);
             for (int i = 0; i < n; ++i) v[i] = i;
@@ -1328,6 +1395,10 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
                     conv_forward<3>(c, a, n, c->d.max_batch);
                 } else if (kind == 7) {
                     conv_wgrad<3>(c, a, n, c->d.max_batch);
+                } else if (kind == 8) {  // conv1 weight gradient + its reduction (fused update)
+                    conv_wgrad<1>(c, a, n, c->d.max_batch);
+                } else if (kind == 9) {
+                    conv_forward<1>(c, a, n, c->d.max_batch);
                 } else if (c->d.gemm_mode == SMX_GEMM_TC) {  // the implicit GEMM alone (no split reduction)
                     using G = cnn::Geo<2>;
                     const int splits = (c->d.max_batch * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
