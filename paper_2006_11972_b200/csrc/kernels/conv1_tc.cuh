@@ -1,33 +1,38 @@
-// conv1 weight gradient on the tensor cores (tensor-core mode; replaces the FFMA2 kernel
-// conv1_wgrad_lane, which ran the FMA pipe at ~57 % and read dA1 at ~2.8 TB/s).
+// conv1 on the tensor cores (tensor-core mode).  conv1 (3x3, 3 -> 32, stride 1) has K = 27 and
+// N = 32, far too thin for a 128-row tile in its natural im2col form; both kernels here reshape it.
 //
-// conv1 (3x3, 3 -> 32, stride 1) has K = 27 and N = 32, far too thin for a 128-row tile in its
-// natural im2col form.  A row shift turns it into a tile that is 75 % dense:
+// ---------------------------------------------------------------------------------------------
+// Weight gradient (replaces the FFMA2 kernel conv1_wgrad_lane, FMA-pipe bound at ~57 %):
 //
 //   dW1[co][kh][kw][ci] = sum_{n, h, w} dA1[n][h][w][co] * X[n][h + kh - 1][w + kw - 1][ci]
-//                       = sum_{n, h', w} dA1[n][h' - kh + 1][w][co] * X[n][h'][w + kw - 1][ci]
 //
-// so with the reduction index k = (n, h', w) (one 32-pixel image row h' per K chunk):
-//   A[(kh, co)][k] = dA1[n][h' - kh + 1][w][co]     M = 3 x 32 = 96 of 128 TMEM lanes (lane 32 kh + co)
-//   B[(kw, ci)][k] = X[n][h'][w + kw - 1][ci]        N = 12 (+ the all-ones row 12 = the bias gradient, from kh = 1)
-//   D[(kh, co)][(kw, ci)] = dW1[co][kh][kw][ci]       M = 128, N = 16, K = 32 per chunk: 4 k-steps
-//
-// Roles (384 threads, 2 CTAs per SM: 256 TMEM columns and ~52 KB of shared memory each):
-//   warp 7      TMA: per image row, one 4 KB bulk copy of the dA1 row + one 512 B copy of the X row
-//               into an 8-entry ring (every row is loaded once and read by three chunks)
-//   warps 0-2   A builders of the even chunks, 4-6 of the odd ones (warp % 4 = kh = TMEM lane
-//               quadrant, lane = co): the chunk's dA1 row
-//               h' - kh + 1 from the ring (zero outside the image), hi = the value (the MMA
-//               truncates to tf32) and lo = a - trunc(a), tcgen05.st into a 3-slot TMEM ring
-//   warp 3      B builder (lane = w): the X row's shifted copies into a K-major SWIZZLE_NONE tile
-//               (LBO 272 B: conflict-free stores), lo tile too when the data is not tf32-exact
-//   warp 11     MMA: 4 k-steps x (A_lo B_hi [, A_hi B_lo], A_hi B_hi) per chunk, kind::tf32
-//   warps 8-10  epilogue (quadrant kh): drain a 16-column accumulator every kSeg chunks (128
-//               products per TMEM segment, §3b.5), fp32 round-to-nearest sums in registers, and
-//               at the end of an item (kImgs images of one slot) the per-item partial row
-//               part[item][co * 28 + (kh * 3 + kw) * 3 + ci] (+ 27: bias) that conv1_wgrad_reduce sums.
-// Work items (slot, group of kImgs images) are walked by a persistent grid; every role walks the
-// same sequence, so ring / slot / segment counters run on across items and images.
+// A K chunk is 4 consecutive image rows h0 .. h0 + 3 of one sample (128 pixels); within it the
+// reduction index is the column w (32 per row).  The four rows sit in the four TMEM lane quadrants
+// of A and in four diagonal blocks of B:
+//   A[(b, co)][w]            = dA1[n][h0 + b][w][co]                    M = 4 rows x 32 co = 128
+//   B[(b, kh, kw, ci)][w]    = X[n][h0 + b + kh - 1][w + kw - 1][ci]     N = 4 blocks x 48 = 192
+//                              (per block 36 taps x channels incl. the zero channel, the all-ones
+//                              bias row 36, rows 37-47 zero: blocks start at 16-column multiples)
+//   D[(b, co)][(b, ...)]     = row h0 + b's contribution to dW1[co][...]  (only the diagonal
+//                              blocks are read: 1/4 of the MMA's columns, but every A element is
+//                              read once per k-step by an N = 160 MMA instead of three times by
+//                              N = 16 MMAs -- an A-from-TMEM MMA costs ~25 + 0.3 N cycles)
+// Roles (384 threads, one CTA per SM, all 512 TMEM columns):
+//   warp 6      TMA: per chunk the 4 dA1 rows (16 KB, contiguous) + the input rows h0 - 1 .. h0 + 4
+//               (clipped to the image) into a 4-entry ring
+//   warps 0-3   A builders (warp b = TMEM lane quadrant, lane = co): dA1 row h0 + b, hi = the value
+//               (the MMA truncates to tf32) and lo = a - trunc(a), tcgen05.st into a 2-slot ring
+//   warps 4-5   B builders (lane = w): blocks 2 (warp - 4) and 2 (warp - 4) + 1, the shifted input
+//               rows into a K-major SWIZZLE_NONE tile (LBO 3088 B: conflict-free stores); lo
+//               tiles too when the data is not tf32-exact
+//   warp 7      MMA: 4 k-steps x (A_lo B_hi [, A_hi B_lo], A_hi B_hi) per chunk, N = 192
+//   warps 8-11  epilogue (quadrant b): drain the block's 37 columns every kSeg chunks (128 products
+//               per TMEM segment, §3b.5), fp32 round-to-nearest sums in registers; at the end of a
+//               work item (kImgs samples of one slot) the four blocks are added in order b = 0..3
+//               into the item's partial row part[item][co * 28 + (kh * 3 + kw) * 3 + ci] (+ 27: bias)
+//               that conv1_wgrad_reduce sums.
+// Work items (slot, group of kImgs samples) are walked by a persistent grid; every role walks the
+// same sequence, so ring / slot / segment counters run on across items.
 #pragma once
 
 #include "conv_ws.cuh"
@@ -43,29 +48,29 @@ using ws::mma_commit_e;
 using ws::tmem_ld16;
 using ws::tmem_st16;
 
-constexpr int kImgs = 4;                       // images per work item (= per partial row)
-constexpr int kRing = 8;                       // image-row ring entries
-constexpr int kRowBytes = 32 * 32 * 4;         // dA1 row: 32 pixels x 32 channels
-constexpr int kXBytes = 32 * 4 * 4;            // X row: 32 pixels x 4 channels (NHWC4)
-constexpr int kEntry = kRowBytes + kXBytes;    // 4608
-constexpr int kASlots = 3, kBSlots = 3;
-constexpr int kLbo = 272, kSbo = 128;          // B tile: (r, k) at (k/4)*272 + (r/8)*128 + (r%8)*16 + (k%4)*4
-constexpr int kBTile = 8 * kLbo;               // 2176 (16 rows x 32 k)
-constexpr int kBOff = kRing * kEntry;          // 36864
-constexpr int kBarOff = kBOff + kBSlots * 2 * kBTile;
-constexpr int kSmem = kBarOff + 512;
-constexpr int kAccCol = kASlots * 64;          // TMEM: [0, 192) A slots (hi +0, lo +32), [192, 224) two accumulators
-constexpr int kTmemCols = 256;
-// warps 0-2 / 4-6: A builders of even / odd chunks (quadrant = warp % 4), 3: B builder, 7: TMA,
-// 8-10: epilogue (quadrants 0-2), 11: MMA
-constexpr int kTmaWarp = 7, kMmaWarp = 11, kEpiWarp0 = 8;
+constexpr int kImgs = 4;                       // samples per work item (= per partial row)
+constexpr int kRing = 4;                       // chunk ring entries
+constexpr int kDBytes = 4 * 32 * 32 * 4;       // 4 dA1 rows: 16 KB
+constexpr int kXRows = 6;                      // input rows h0 - 1 .. h0 + 4
+constexpr int kEntry = kDBytes + kXRows * 512;  // 19456
+constexpr int kASlots = 2, kBSlots = 2;
+constexpr int kN = 192, kBlk = 48;            // blocks start at 16-column multiples
+constexpr int kLbo = 3088, kSbo = 128;         // B tile: (r, k) at (k/4)*3088 + (r/8)*128 + (r%8)*16 + (k%4)*4
+constexpr int kBTile = 8 * kLbo;               // 24704 (192 rows x 32 k)
+constexpr int kBOff = kRing * kEntry;          // 77824
+constexpr int kRedOff = kBOff + kBSlots * 2 * kBTile;  // 176640: item-end block sums [4][32][48]
+constexpr int kBarOff = kRedOff + 4 * 32 * kBlk * 4;   // 201216
+constexpr int kSmem = kBarOff + 256;
+constexpr int kAccCol = kASlots * 64;          // TMEM: [0, 128) A slots (hi +0, lo +32), [128, 512) two accumulators
+constexpr int kTmemCols = 512;
+constexpr int kTmaWarp = 6, kMmaWarp = 7, kEpiWarp0 = 8;
 constexpr int kThreads = 12 * 32;
 constexpr int kSeg = SMX_SEG_CHUNKS;
-static_assert(kAccCol + 32 <= kTmemCols, "TMEM plan");
-static_assert((32 * kImgs) % kSeg == 0, "segments tile an item");
+static_assert(kAccCol + 2 * kN <= kTmemCols, "TMEM plan");
+static_assert(kSmem <= 227 * 1024, "shared-memory plan");
 
 struct Item {
-    int slot, part, n0, n1;  // images [n0, n1) of slot
+    int slot, part, n0, n1;  // samples [n0, n1) of slot
 };
 __device__ __forceinline__ bool item_at(const ConvArgs& p, int j, int parts, Item& it) {
     const int z = j / parts;
@@ -77,14 +82,16 @@ __device__ __forceinline__ bool item_at(const ConvArgs& p, int j, int parts, Ite
     return it.n0 < it.n1;
 }
 
+__device__ __forceinline__ int boff(int r, int k) { return ((k >> 2) * kLbo + (r >> 3) * kSbo + (r & 7) * 16) / 4 + (k & 3); }
+
 template <bool XEXACT>
-__global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p, int parts, int nitems) {
+__global__ void __launch_bounds__(kThreads, 1) conv1_wgrad_tc_kernel(ConvArgs p, int parts, int nitems) {
     extern __shared__ __align__(1024) char smem[];
     uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + kBarOff);  // ring entry landed (tx)
-    uint64_t* rempty = rfull + kRing;                               // entry read by its 4 consumers
-    uint64_t* afull = rempty + kRing;                               // A slot written (96 threads)
+    uint64_t* rempty = rfull + kRing;                               // entry read by the 6 builder warps
+    uint64_t* afull = rempty + kRing;                               // A slot written (128 threads)
     uint64_t* aempty = afull + kASlots;                             // A slot's MMAs done
-    uint64_t* bfull = aempty + kASlots;                             // B tile written
+    uint64_t* bfull = aempty + kASlots;                             // B tile written (2 warps)
     uint64_t* bempty = bfull + kBSlots;                             // B tile's MMAs done
     uint64_t* accf = bempty + kBSlots;                              // accumulator segment done
     uint64_t* acce = accf + 2;                                      // accumulator drained
@@ -96,34 +103,33 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p,
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (warp == 3) {  // constant B rows: ci = 3 (the zero input channel) rows 3 / 7 / 11, the ones row 12, rows 13-15
-        for (int b = 0; b < 2 * kBSlots; ++b) {
-            float* t = reinterpret_cast<float*>(smem + kBOff + b * kBTile);
-            const int k = lane;
-            for (int r = 3; r < 16; ++r) {
-                if (r != 3 && r != 7 && r < 11) continue;
-                const float v = (r == 12 && b % 2 == 0) ? 1.0f : 0.0f;  // the lo tile's ones row is 0
-                t[((k >> 2) * kLbo + (r >> 3) * kSbo + (r & 7) * 16) / 4 + (k & 3)] = v;
-            }
+    if (warp == 4 || warp == 5) {  // constant B rows: the zero channel, the ones rows, rows 37-39
+        for (int t = 0; t < 2 * kBSlots; ++t) {
+            float* bt = reinterpret_cast<float*>(smem + kBOff + t * kBTile);
+            for (int b = 2 * (warp - 4); b < 2 * (warp - 4) + 2; ++b)
+                for (int i = 0; i < kBlk; ++i) {
+                    if (i < 36 && (i & 3) != 3) continue;
+                    bt[boff(b * kBlk + i, lane)] = (i == 36 && t % 2 == 0) ? 1.0f : 0.0f;  // lo tiles: 0
+                }
         }
         asm volatile("fence.proxy.async.shared::cta;");
     }
     if (threadIdx.x == 0) {
         for (int e = 0; e < kRing; ++e) {
             mbar_init(&rfull[e], 1);
-            mbar_init(&rempty[e], 4);
+            mbar_init(&rempty[e], 6);
         }
         for (int a = 0; a < kASlots; ++a) {
-            mbar_init(&afull[a], 96);
+            mbar_init(&afull[a], 128);
             mbar_init(&aempty[a], 1);
         }
         for (int b = 0; b < kBSlots; ++b) {
-            mbar_init(&bfull[b], 1);
+            mbar_init(&bfull[b], 2);
             mbar_init(&bempty[b], 1);
         }
         for (int u = 0; u < 2; ++u) {
             mbar_init(&accf[u], 1);
-            mbar_init(&acce[u], 96);
+            mbar_init(&acce[u], 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -133,109 +139,88 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p,
     const uint32_t tmem = *tmem_slot;
     Item it;
 
-    if (warp < 7 && warp != 3) {
-        // ================= A builders: warp kh (+ 4 for odd chunks), lane co =================
-        const int kh = warp & 3, set = warp >> 2;
-        const uint32_t tq = tmem + ((uint32_t)(kh * 32) << 16);
-        int g = 0;  // chunks (= image rows) of this CTA
+    if (warp < 4) {
+        // ================= A builders: warp b = row h0 + b, lane co =================
+        const int b = warp;
+        const uint32_t tq = tmem + ((uint32_t)(b * 32) << 16);
+        int g = 0;  // chunks of this CTA
         for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
             if (!item_at(p, j, parts, it)) continue;
-            for (int n = it.n0; n < it.n1; ++n) {
-                const int gb = g;  // global row index of this image's row 0
-                for (int h = 0; h < 32; ++h, ++g) {
-                    if ((g & 1) != set) continue;
-                    const int a = g % kASlots;
-                    if (g >= kASlots) mbar_wait(&aempty[a], ((g / kASlots) - 1) & 1);
-                    const int row = h - kh + 1;
-                    const int gr = gb + row, e = gr % kRing;
-                    float x[32];
-                    if ((unsigned)row < 32u) {
-                        mbar_wait(&rfull[e], (gr / kRing) & 1);
-                        const float* src = reinterpret_cast<const float*>(smem + e * kEntry) + lane;
+            for (int c = 0; c < (it.n1 - it.n0) * 8; ++c, ++g) {
+                const int a = g % kASlots, e = g % kRing;
+                if (g >= kASlots) mbar_wait(&aempty[a], ((g / kASlots) - 1) & 1);
+                mbar_wait(&rfull[e], (g / kRing) & 1);
+                const float* src = reinterpret_cast<const float*>(smem + e * kEntry) + b * 1024 + lane;
+                float x[32];
 #pragma unroll
-                        for (int w = 0; w < 32; ++w) x[w] = src[w * 32];
-                    } else {
+                for (int w = 0; w < 32; ++w) x[w] = src[w * 32];
+                const uint32_t ta = tq + a * 64;
+                tmem_st16(ta, x);
+                tmem_st16(ta + 16, x + 16);
+                float lo[32];
 #pragma unroll
-                        for (int w = 0; w < 32; ++w) x[w] = 0.0f;
-                    }
-                    const uint32_t ta = tq + a * 64;
-#ifndef C1_DBG_NO_AST  // profiling variant: no A stores
-                    tmem_st16(ta, x);
-                    tmem_st16(ta + 16, x + 16);
-                    float lo[32];
-#pragma unroll
-                    for (int w = 0; w < 32; ++w) lo[w] = lo_of(x[w]);
-                    tmem_st16(ta + 32, lo);
-                    tmem_st16(ta + 48, lo + 16);
-#else
-                    if (x[0] == 12345.0f && x[31] == 1.0f) tmem_st16(ta, x);
-#endif
-                    asm volatile("tcgen05.wait::st.sync.aligned;");
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&afull[a]);
-                    __syncwarp();
-                    // release the ring entry (its values are consumed); rows no chunk of this warp
-                    // reads (row 0 for kh = 0, row 31 for kh = 2) are released once they landed
-                    if (lane == 0) {
-                        if ((unsigned)row < 32u) mbar_arrive(&rempty[e]);
-                        if (kh == 0 && h == 0) {
-                            mbar_wait(&rfull[gb % kRing], (gb / kRing) & 1);
-                            mbar_arrive(&rempty[gb % kRing]);
-                        }
-                        if (kh == 2 && h == 31) {
-                            const int gl = gb + 31;
-                            mbar_wait(&rfull[gl % kRing], (gl / kRing) & 1);
-                            mbar_arrive(&rempty[gl % kRing]);
-                        }
-                    }
-                    __syncwarp();
-                }
+                for (int w = 0; w < 32; ++w) lo[w] = lo_of(x[w]);
+                tmem_st16(ta + 32, lo);
+                tmem_st16(ta + 48, lo + 16);
+                asm volatile("tcgen05.wait::st.sync.aligned;");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                mbar_arrive(&afull[a]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&rempty[e]);
             }
         }
-    } else if (warp == 3) {
-        // ================= B builder: lane w =================
+    } else if (warp < 6) {
+        // ================= B builders: lane w, blocks 2 (warp - 4) .. + 1 =================
+        const int b0 = 2 * (warp - 4);
         int g = 0;
         for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
             if (!item_at(p, j, parts, it)) continue;
-            for (int n = it.n0; n < it.n1; ++n) {
-                for (int h = 0; h < 32; ++h, ++g) {
-                    const int b = g % kBSlots, e = g % kRing;
-                    mbar_wait(&rfull[e], (g / kRing) & 1);
-                    if (g >= kBSlots) mbar_wait(&bempty[b], ((g / kBSlots) - 1) & 1);
-                    const float4 xc = reinterpret_cast<const float4*>(smem + e * kEntry + kRowBytes)[lane];
-                    float4 xl, xr;  // pixels w - 1 and w + 1 (zero padding at the image edges)
+            for (int c = 0; c < (it.n1 - it.n0) * 8; ++c, ++g) {
+                const int s = g % kBSlots, e = g % kRing, h0 = (c & 7) * 4;
+                mbar_wait(&rfull[e], (g / kRing) & 1);
+                if (g >= kBSlots) mbar_wait(&bempty[s], ((g / kBSlots) - 1) & 1);
+                const float4* xr = reinterpret_cast<const float4*>(smem + e * kEntry + kDBytes);
+                float* hi = reinterpret_cast<float*>(smem + kBOff + (2 * s) * kBTile);
+                // input rows h0 + b0 - 1 .. h0 + b0 + 2 feed blocks b0, b0 + 1 (entry row = ih - h0 + 1)
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int ih = h0 + b0 - 1 + rr;
+                    float4 xc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if ((unsigned)ih < 32u) xc = xr[(ih - h0 + 1) * 32 + lane];
+                    float4 xl, xq;
                     xl.x = __shfl_up_sync(0xffffffffu, xc.x, 1);
                     xl.y = __shfl_up_sync(0xffffffffu, xc.y, 1);
                     xl.z = __shfl_up_sync(0xffffffffu, xc.z, 1);
-                    xr.x = __shfl_down_sync(0xffffffffu, xc.x, 1);
-                    xr.y = __shfl_down_sync(0xffffffffu, xc.y, 1);
-                    xr.z = __shfl_down_sync(0xffffffffu, xc.z, 1);
+                    xq.x = __shfl_down_sync(0xffffffffu, xc.x, 1);
+                    xq.y = __shfl_down_sync(0xffffffffu, xc.y, 1);
+                    xq.z = __shfl_down_sync(0xffffffffu, xc.z, 1);
                     if (lane == 0) xl = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (lane == 31) xr = make_float4(0.f, 0.f, 0.f, 0.f);
-                    const float v[9] = {xl.x, xl.y, xl.z, xc.x, xc.y, xc.z, xr.x, xr.y, xr.z};  // (kw, ci)
-                    float* hi = reinterpret_cast<float*>(smem + kBOff + (2 * b) * kBTile);
-                    const int kofs = ((lane >> 2) * kLbo) / 4 + (lane & 3);
+                    if (lane == 31) xq = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float v[9] = {xl.x, xl.y, xl.z, xc.x, xc.y, xc.z, xq.x, xq.y, xq.z};  // (kw, ci)
 #pragma unroll
-                    for (int kw = 0; kw < 3; ++kw)
+                    for (int bb = 0; bb < 2; ++bb) {
+                        const int kh = rr - bb;  // block b0 + bb reads input row h0 + b0 + bb + kh - 1
+                        if (kh < 0 || kh > 2) continue;
 #pragma unroll
-                        for (int ci = 0; ci < 3; ++ci) {
-                            const int r = kw * 4 + ci;
-                            hi[kofs + ((r >> 3) * kSbo + (r & 7) * 16) / 4] = v[kw * 3 + ci];
-                            if constexpr (!XEXACT)
-                                hi[kBTile / 4 + kofs + ((r >> 3) * kSbo + (r & 7) * 16) / 4] = lo_of(v[kw * 3 + ci]);
-                        }
-                    asm volatile("fence.proxy.async.shared::cta;");  // generic stores -> the MMA's async proxy
-                    __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&bfull[b]);
-                        mbar_arrive(&rempty[e]);
+                        for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+                            for (int ci = 0; ci < 3; ++ci) {
+                                const int r = (b0 + bb) * kBlk + (kh * 3 + kw) * 4 + ci;
+                                hi[boff(r, lane)] = v[kw * 3 + ci];
+                                if constexpr (!XEXACT) hi[kBTile / 4 + boff(r, lane)] = lo_of(v[kw * 3 + ci]);
+                            }
                     }
-                    __syncwarp();
+                }
+                asm volatile("fence.proxy.async.shared::cta;");  // generic stores -> the MMA's async proxy
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&bfull[s]);
+                    mbar_arrive(&rempty[e]);
                 }
             }
         }
     } else if (warp == kTmaWarp) {
-        // ================= TMA: dA1 row + X row per ring entry =================
+        // ================= TMA: 4 dA1 rows + the input rows per chunk =================
         if (lane == 0) {
             int g = 0;
             for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
@@ -243,35 +228,34 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p,
                 const SlotView v = slot_view(p, it.slot);
                 const float* dy = layer_dout<1>(p, v);
                 const float* x = layer_in<1>(p, v);
-                for (int n = it.n0; n < it.n1; ++n)
-                    for (int h = 0; h < 32; ++h, ++g) {
-                        const int e = g % kRing;
-                        if (g >= kRing) mbar_wait(&rempty[e], ((g / kRing) - 1) & 1);
-                        ws::mbar_arrive_expect_tx(&rfull[e], kEntry);
-                        ws::bulk_g2s(smem + e * kEntry, dy + ((long long)n * 1024 + h * 32) * 32, kRowBytes, &rfull[e]);
-                        ws::bulk_g2s(smem + e * kEntry + kRowBytes, x + (long long)n * kSample + h * 128, kXBytes,
-                                     &rfull[e]);
-                    }
+                for (int c = 0; c < (it.n1 - it.n0) * 8; ++c, ++g) {
+                    const int e = g % kRing, n = it.n0 + (c >> 3), h0 = (c & 7) * 4;
+                    if (g >= kRing) mbar_wait(&rempty[e], ((g / kRing) - 1) & 1);
+                    const int r0 = max(0, h0 - 1), r1 = min(32, h0 + 5);
+                    ws::mbar_arrive_expect_tx(&rfull[e], kDBytes + (r1 - r0) * 512);
+                    ws::bulk_g2s(smem + e * kEntry, dy + ((long long)n * 1024 + h0 * 32) * 32, kDBytes, &rfull[e]);
+                    ws::bulk_g2s(smem + e * kEntry + kDBytes + (r0 - h0 + 1) * 512, x + (long long)n * kSample + r0 * 128,
+                                 (r1 - r0) * 512, &rfull[e]);
+                }
             }
         }
         __syncwarp();
     } else if (warp == kMmaWarp) {
         // ================= MMA issuer =================
-        const uint32_t idesc = idesc_tf32(16);
+        const uint32_t idesc = idesc_tf32(kN);
         int g = 0, sg = 0;
         for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
             if (!item_at(p, j, parts, it)) continue;
-            const int nch = (it.n1 - it.n0) * 32;
+            const int nch = (it.n1 - it.n0) * 8;
             for (int c = 0; c < nch; ++c, ++g) {
-                const int a = g % kASlots, b = g % kBSlots, buf = sg & 1;
-                const bool seg_start = c % kSeg == 0, seg_end = c % kSeg == kSeg - 1;
+                const int a = g % kASlots, s = g % kBSlots, buf = sg & 1;
+                const bool seg_start = c % kSeg == 0, seg_end = c % kSeg == kSeg - 1 || c == nch - 1;
                 if (seg_start && sg >= 2) mbar_wait(&acce[buf], ((sg >> 1) - 1) & 1);
                 mbar_wait(&afull[a], (g / kASlots) & 1);
-                mbar_wait(&bfull[b], (g / kBSlots) & 1);
+                mbar_wait(&bfull[s], (g / kBSlots) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t d = tmem + kAccCol + buf * 16, ah = tmem + a * 64, al = ah + 32;
-                const uint32_t bh = smem_u32(smem + kBOff + (2 * b) * kBTile), bl = bh + kBTile;
-#ifndef C1_DBG_NO_MMA  // profiling variant: commits only
+                const uint32_t d = tmem + kAccCol + buf * kN, ah = tmem + a * 64, al = ah + 32;
+                const uint32_t bh = smem_u32(smem + kBOff + (2 * s) * kBTile), bl = bh + kBTile;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const uint64_t dh = smem_desc(bh + 2 * k * kLbo, kLbo, kSbo);
@@ -280,11 +264,8 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p,
                     if constexpr (!XEXACT) ws::mma_ts_e(d, ah + 8 * k, smem_desc(bl + 2 * k * kLbo, kLbo, kSbo), idesc, 1u);
                     ws::mma_ts_e(d, ah + 8 * k, dh, idesc, 1u);
                 }
-#else
-                (void)d; (void)ah; (void)al; (void)bh; (void)bl; (void)idesc;
-#endif
                 mma_commit_e(&aempty[a]);
-                mma_commit_e(&bempty[b]);
+                mma_commit_e(&bempty[s]);
                 if (seg_end) {
                     mma_commit_e(&accf[buf]);
                     ++sg;
@@ -293,41 +274,52 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_wgrad_tc_kernel(ConvArgs p,
         }
         __syncwarp();
     } else {
-        // ================= epilogue: warp 8 + kh, lane co =================
-        const int kh = warp - kEpiWarp0;
-        const uint32_t tq = tmem + ((uint32_t)(kh * 32) << 16) + kAccCol;
+        // ================= epilogue: warp 8 + b, lane co =================
+        const int b = warp - kEpiWarp0;
+        const uint32_t tq = tmem + ((uint32_t)(b * 32) << 16) + kAccCol + b * kBlk;
+        float* red = reinterpret_cast<float*>(smem + kRedOff);
+        const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
         int sg = 0;
         for (int j = blockIdx.x; j < nitems; j += gridDim.x) {
             if (!item_at(p, j, parts, it)) continue;
-            const int nseg = (it.n1 - it.n0) * 32 / kSeg;
-            float sum[16];
+            const int nseg = ((it.n1 - it.n0) * 8 + kSeg - 1) / kSeg;
+            float sum[37];
             for (int s = 0; s < nseg; ++s, ++sg) {
                 const int buf = sg & 1;
                 mbar_wait(&accf[buf], (sg >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                uint32_t r[16];
-                tmem_ld16(tq + buf * 16, r);
+                uint32_t r[kBlk];
+                tmem_ld16(tq + buf * kN, r);
+                tmem_ld16(tq + buf * kN + 16, r + 16);
+                ws::tmem_ld16(tq + buf * kN + 32, r + 32);
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 mbar_arrive(&acce[buf]);
 #pragma unroll
-                for (int c = 0; c < 16; ++c)
-                    sum[c] = s == 0 ? __uint_as_float(r[c]) : __fadd_rn(sum[c], __uint_as_float(r[c]));
+                for (int q = 0; q < 37; ++q)
+                    sum[q] = s == 0 ? __uint_as_float(r[q]) : __fadd_rn(sum[q], __uint_as_float(r[q]));
             }
+            // the four row blocks' sums, added in order b = 0..3
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the previous item's reads of red are done
+#pragma unroll
+            for (int q = 0; q < 37; ++q) red[(b * 32 + lane) * kBlk + q] = sum[q];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             const SlotView v = slot_view(p, it.slot);
-            float* part = v.act + p.al.w1p + (long long)it.part * kL1Outs + lane * 28;
+            float* part = v.act + p.al.w1p + (long long)it.part * kL1Outs;
+            for (int i = et; i < kL1Outs; i += 128) {
+                const int co = i / 28, jj = i % 28;
+                const int q = jj < 27 ? (jj / 3) * 4 + jj % 3 : 36;
+                float t = red[co * kBlk + q];
 #pragma unroll
-            for (int kw = 0; kw < 3; ++kw)
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci) part[(kh * 3 + kw) * 3 + ci] = sum[kw * 4 + ci];
-            if (kh == 1) part[27] = sum[12];
+                for (int bb = 1; bb < 4; ++bb) t = __fadd_rn(t, red[(bb * 32 + co) * kBlk + q]);
+                part[i] = t;
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
-
 
 // ---------------------------------------------------------------------------------------------
 // conv1 forward on the tensor cores (tensor-core mode; replaces the FFMA2 kernel conv1_fwd_lane,

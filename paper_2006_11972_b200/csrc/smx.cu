@@ -339,8 +339,8 @@ void wgrad2_at(smx_ctx* c, const cnn::ConvArgs& a, int splits, int groups) {
     launch_check(c, "wgrad2_at");
 }
 
-// conv1 weight gradient on the tensor cores (kernels/conv1_tc.cuh): persistent grid, 2 CTAs per SM,
-// one work item per (slot, group of kImgs samples) -> one partial row each
+// conv1 weight gradient on the tensor cores (kernels/conv1_tc.cuh): persistent grid, one CTA per
+// SM, one work item per (slot, group of kImgs samples) -> one partial row each
 void conv1_wgrad_tc(smx_ctx* c, const cnn::ConvArgs& a, int mb, int groups) {
     namespace c1 = cnn::c1;
     static unsigned long long configured = 0;
@@ -353,7 +353,7 @@ void conv1_wgrad_tc(smx_ctx* c, const cnn::ConvArgs& a, int mb, int groups) {
         configured |= bit;
     }
     const int parts = (mb + c1::kImgs - 1) / c1::kImgs, items = parts * groups;
-    const int grid = std::min(items, 2 * c->num_sms);
+    const int grid = std::min(items, c->num_sms);  // one CTA per SM (all 512 TMEM columns)
     if (c->data_tf32_exact)
         c1::conv1_wgrad_tc_kernel<true><<<grid, c1::kThreads, c1::kSmem, c->cur>>>(a, parts, items);
     else
