@@ -409,7 +409,8 @@ def main():
     kx.sync()
     # CNN: 2 / 3 = conv2 forward / weight gradient, 4 / 5 = conv2 / conv3 input gradient, 6 = conv3
     # forward, 7 = conv3 weight gradient (+ its split reduction); MLP: 2 / 3 only
-    ms = {kind: kx.bench_kernel(kind, n_k, 30) for kind in ((2, 3, 4, 5, 6, 7) if cnn else (2, 3))}
+    # 8 / 9 = conv1 weight gradient (+ reduction) / forward, both HBM-bound tensor-core kernels
+    ms = {kind: kx.bench_kernel(kind, n_k, 30) for kind in ((2, 3, 4, 5, 6, 7, 8, 9) if cnn else (2, 3))}
     # HBM-bound kernels on a working set > 3x the 126 MB L2 (many small slots / checkpoints)
     n_h = int(np.ceil(3 * 126e6 / (20 * kx.p_algo * 1.0) / 16)) * 16
     kh = ex.Executor(n_slots=n_h, n_ckpts=n_h, device=local, max_steps=8, gemm_mode=gemm_mode, max_batch=8,
@@ -453,6 +454,10 @@ def main():
             "K2_conv3_dgrad": tensor("dgrad3", gemm_flops, ms[5]),
             "K1_conv3_fwd": tensor("fwd3", gemm_flops, ms[6]),
             "K3_conv3_wgrad": tensor("wgrad3", gemm_flops, ms[7]),
+            # conv1 (tensor cores, HBM-bound): the forward writes a1 (128 x 1024 x 32 fp32 per slot)
+            # and reads the images (128 x 4096 fp32); the weight gradient reads dA1 and the images
+            "K1_conv1_fwd": hbm("fwd1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[9]),
+            "K3_conv1_wgrad": hbm("wgrad1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[8]),
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }
