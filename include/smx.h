@@ -158,7 +158,8 @@ int smx_reset_stats(smx_ctx* ctx);
  * 3 = the layer-1 weight-gradient GEMM over `n` slots (both at the slots' current batch size);
  * for the CNN, 2 = the conv2 forward implicit GEMM and 3 = the conv2 weight-gradient implicit
  * GEMM (tensor-core mode: the split GEMM alone; exact mode: the SIMT kernel); 4 / 5 = the conv2 /
- * conv3 input gradient, 6 = the conv3 forward, 7 = the conv3 weight gradient (with its reduction),
+ * conv3 input gradient, 6 = the conv3 forward, 7 = the conv3 weight gradient (tensor-core mode: the
+ * split GEMM alone; exact mode: with its reduction),
  * 8 = the conv1 weight gradient (with its reduction), 9 = the conv1 forward.
  * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);

@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(256) conv_dgrad_simt(ConvArgs p) {
 // ---- head (both modes): pool + FC + softmax-CE, loss, FC grads, dA3 --------------------------
 // grid (max_batch, groups), block 128: one sample per block.
 // g[c] = (sum_{p asc} a3[p][c]) * 2^-6;  z[k] = fmaf chain over c of g[c]*W4[k][c], + b4[k]
-// train: dz = (softmax - onehot) / B, row loss;  eval (zout != null): logits to zout.
+// train: dz = (softmax - onehot) / B, row loss, then the sample's dA3 (pool / ReLU backward);
+// eval (zout != null): logits to zout.
 __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const int n = blockIdx.x;
@@ -421,15 +422,34 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
         if (p.zout) p.zout[p.z_stride * blockIdx.y + ((long long)p.x_row0 + n) * kNCP + c] = z[c];
     }
     __syncthreads();
-    if (!p.zout && c == 0) {
+    if (p.zout) return;
+    __shared__ float dzs[kNCP];
+    if (c == 0) {
         const int y = p.labels[conv_row0(p, v.slot) + n];
         float dz[kNC];
         const float l = softmax_ce_row(z, y, dz, nullptr);
         v.act[p.al.rl + n] = l;
         float* dzo = v.act + p.al.dz + (long long)n * kNCP;
         const float fb = (float)v.bs;
-        for (int k = 0; k < kNC; ++k) dzo[k] = __fdiv_rn(dz[k], fb);
-        for (int k = kNC; k < kNCP; ++k) dzo[k] = 0.0f;
+        for (int k = 0; k < kNC; ++k) dzs[k] = dzo[k] = __fdiv_rn(dz[k], fb);
+        for (int k = kNC; k < kNCP; ++k) dzs[k] = dzo[k] = 0.0f;
+    }
+    __syncthreads();
+    // the pool / ReLU backward of this sample (formerly head_dg_kernel, same arithmetic):
+    // dg[c] = (fmaf chain over k < 16 of dz * W4[k][c]) * 2^-6; d3[n][p][c] = (a3 > 0) ? dg[c] : 0
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kNCP; ++k) acc = __fmaf_rn(dzs[k], v.w[kOffW4 + k * kFeat + c], acc);
+    const float dg = __fmul_rn(acc, 0.015625f);
+    float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
+    if (p.pooled) {  // a3 > 0 as the bitmap the conv3 forward epilogue wrote: word (n, pix, c / 32)
+        const uint32_t* mk = reinterpret_cast<const uint32_t*>(v.act + p.al.mk3) + (long long)n * 64 * (kFeat / 32) + c / 32;
+#pragma unroll 16
+        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = (__ldg(mk + pix * (kFeat / 32)) >> (c & 31)) & 1u ? dg : 0.0f;
+    } else {
+        const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
+#pragma unroll 16
+        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
     }
 }
 
@@ -459,30 +479,6 @@ __global__ void __launch_bounds__(128) head_grad_kernel(ConvArgs p) {
         float s = 0.0f;
         for (int n = 0; n < v.bs; ++n) s = __fadd_rn(s, v.act[p.al.rl + n]);
         p.loss_hist[(long long)v.slot * p.hp_cap + p.st[v.slot].step] = __fdiv_rn(s, (float)v.bs);
-    }
-}
-
-// grid (max_batch, groups), block 128: dg[c] = (fmaf chain over k < 16 of dz*W4[k][c]) * 2^-6;
-// d3[n][p][c] = (a3 > 0) ? dg[c] : 0
-__global__ void __launch_bounds__(128) head_dg_kernel(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
-    const int n = blockIdx.x;
-    if (n >= v.bs) return;
-    const int c = threadIdx.x;
-    const float* dz = v.act + p.al.dz + (long long)n * kNCP;
-    float acc = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kNCP; ++k) acc = __fmaf_rn(dz[k], v.w[kOffW4 + k * kFeat + c], acc);
-    const float dg = __fmul_rn(acc, 0.015625f);
-    float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
-    if (p.pooled) {  // a3 > 0 as the bitmap the conv3 forward epilogue wrote: word (n, pix, c / 32)
-        const uint32_t* mk = reinterpret_cast<const uint32_t*>(v.act + p.al.mk3) + (long long)n * 64 * (kFeat / 32) + c / 32;
-#pragma unroll 16
-        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = (__ldg(mk + pix * (kFeat / 32)) >> (c & 31)) & 1u ? dg : 0.0f;
-    } else {
-        const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
-#pragma unroll 16
-        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
     }
 }
 
@@ -834,13 +830,13 @@ __device__ __forceinline__ float tf32_rna_h(float x) {
     return __uint_as_float(r);
 }
 template <int L>
-__global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
+__device__ __forceinline__ void weight_image_body(const ConvArgs& p, int bx, int nbx) {
     using G = Geo<L>;
     const SlotView v = slot_view(p, p.slots[blockIdx.y]);
     const float* W = v.w + G::OffW;
     const int fwd_units = WImg<L>::FwdChunks * 8 * G::Co;
     const int dgr_units = (L >= 2) ? WImg<L>::DgrChunks * 8 * WImg<L>::DgrN : 0;
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < fwd_units + dgr_units; u += gridDim.x * blockDim.x) {
+    for (int u = bx * blockDim.x + threadIdx.x; u < fwd_units + dgr_units; u += nbx * blockDim.x) {
         float val[4];
         float* dst;
         int nt;
@@ -882,6 +878,23 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
         *reinterpret_cast<float4*>(dst) = hi;
         *reinterpret_cast<float4*>(dst + nt * 32) = lo;  // lo tile follows the hi tile (nt*128 bytes)
     }
+}
+
+template <int L>
+constexpr int wimg_units() {
+    return WImg<L>::FwdChunks * 8 * Geo<L>::Co + (L >= 2 ? WImg<L>::DgrChunks * 8 * WImg<L>::DgrN : 0);
+}
+constexpr int kWImgBlocks1 = (wimg_units<1>() + 255) / 256, kWImgBlocks2 = (wimg_units<2>() + 255) / 256,
+              kWImgBlocks3 = (wimg_units<3>() + 255) / 256;
+// all three layers' images in one launch: grid (kWImgBlocks1 + 2 + 3, groups), block 256
+__global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
+    const int b = blockIdx.x;
+    if (b < kWImgBlocks1)
+        weight_image_body<1>(p, b, kWImgBlocks1);
+    else if (b < kWImgBlocks1 + kWImgBlocks2)
+        weight_image_body<2>(p, b - kWImgBlocks1, kWImgBlocks2);
+    else
+        weight_image_body<3>(p, b - kWImgBlocks1 - kWImgBlocks2, kWImgBlocks3);
 }
 
 // ---- layer 1 in tensor-core mode: fp32 SIMT kernels ---------------------------------------

@@ -450,15 +450,8 @@ void conv_dgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
 // Pre-split tf32 hi/lo weight images of the three convs (tensor-core mode), see cnn::WImg.
 void weight_images(smx_ctx* c, const cnn::ConvArgs& a, int n) {
     if (c->d.gemm_mode != SMX_GEMM_TC) return;
-    auto blocks = [](int units) { return (unsigned)((units + 255) / 256); };
-    cnn::weight_image_kernel<1><<<dim3(blocks(cnn::WImg<1>::FwdChunks * 8 * 32), n), 256, 0, c->cur>>>(a);
-    launch_check(c, "weight_image 1");
-    cnn::weight_image_kernel<2><<<dim3(blocks(cnn::WImg<2>::FwdChunks * 8 * 64 + cnn::WImg<2>::DgrChunks * 8 * 128), n),
-                                   256, 0, c->cur>>>(a);
-    launch_check(c, "weight_image 2");
-    cnn::weight_image_kernel<3><<<dim3(blocks(cnn::WImg<3>::FwdChunks * 8 * 128 + cnn::WImg<3>::DgrChunks * 8 * 256), n),
-                                   256, 0, c->cur>>>(a);
-    launch_check(c, "weight_image 3");
+    cnn::weight_image_kernel<<<dim3(cnn::kWImgBlocks1 + cnn::kWImgBlocks2 + cnn::kWImgBlocks3, n), 256, 0, c->cur>>>(a);
+    launch_check(c, "weight_image");
 }
 
 // One lockstep of the CNN over `n` slots: forward, head, backward as two branches (input
@@ -472,18 +465,17 @@ void enqueue_lockstep_cnn(smx_ctx* c, const int* d_slots, int n) {
     conv_forward<1>(c, a, n, mb);
     conv_forward<2>(c, a, n, mb);
     conv_forward<3>(c, a, n, mb);
-    cnn::head_fwd_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
+    cnn::head_fwd_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);  // + dA3 (the pool / ReLU backward)
     launch_check(c, "head_fwd");
-    cnn::head_grad_kernel<<<dim3((cnn::kNCP * cnn::kFeat + cnn::kNCP + 127) / 128, n), 128, 0, c->stream>>>(a);
-    launch_check(c, "head_grad");
-    cnn::head_dg_kernel<<<dim3(mb, n), 128, 0, c->stream>>>(a);
-    launch_check(c, "head_dg");
     auto fork = [&](int i) {
         ck(cudaEventRecord(c->fj[i], c->stream), "fork record");
         ck(cudaStreamWaitEvent(c->side, c->fj[i], 0), "fork wait");
     };
     fork(0);
     c->cur = c->side;
+    // FC gradients + the step's loss: only the conv3 weight-gradient reduction (the FC update) reads them
+    cnn::head_grad_kernel<<<dim3((cnn::kNCP * cnn::kFeat + cnn::kNCP + 127) / 128, n), 128, 0, c->side>>>(a);
+    launch_check(c, "head_grad");
     conv_wgrad<3>(c, a, n, mb);
     c->cur = c->stream;
     conv_dgrad<3>(c, a, n, mb);
@@ -1393,6 +1385,10 @@ int smx_bench_kernel(smx_ctx* c, int kind, int n, int reps, double* ms_per_launc
                     conv_dgrad<3>(c, a, n, c->d.max_batch);
                 } else if (kind == 6) {
                     conv_forward<3>(c, a, n, c->d.max_batch);
+                } else if (kind == 7 && c->d.gemm_mode == SMX_GEMM_TC) {  // the implicit GEMM alone
+                    using G = cnn::Geo<3>;
+                    const int splits = (c->d.max_batch * G::OH * G::OH + cnn::kSplitRows - 1) / cnn::kSplitRows;
+                    conv_tc<cnn::ctc::Wgrad<3>>(c, a, splits, cnn::Part<3>::Rows, n);
                 } else if (kind == 7) {
                     conv_wgrad<3>(c, a, n, c->d.max_batch);
                 } else if (kind == 8) {  // conv1 weight gradient + its reduction (fused update)
