@@ -88,6 +88,7 @@ struct smx_ctx {
     struct Graph {
         int* d_slots = nullptr;
         cudaGraphExec_t exec = nullptr;
+        long long launches = 0;  // kernels in the captured lockstep
     };
     std::map<std::vector<int>, Graph> graphs;
     int* scratch_slots = nullptr;  // for non-graph launches
@@ -102,7 +103,6 @@ struct smx_ctx {
     long long act_stride = kActStride;
     long long d_in = kD0;            // floats per input sample
     cnn::ActLayout al{};
-    int lockstep_launches = 14;      // kernels per captured lockstep
     float* zval = nullptr;           // CNN eval logits [kEvalChunk][n_val][16]
     CUtensorMap* tmaps = nullptr;    // CNN: [S][cnn::kTmapKinds] TMA maps of the conv A operands
 
@@ -706,6 +706,7 @@ smx_ctx::Graph& graph_for(smx_ctx* c, const std::vector<int>& slots) {
         cudaStreamEndCapture(c->stream, &graph);
         throw;
     }
+    g.launches = c->stats.launches - launches;
     c->stats.launches = launches;
     ck(cudaStreamEndCapture(c->stream, &graph), "end capture");
     ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
@@ -817,7 +818,6 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
         ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
         c->S = n_slots;
         c->C = n_ckpts;
-        c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 13 : 14;  // MLP (TC: K5 fused)
         if (d.model == SMX_MODEL_CNN) {
             if (d.n_val % d.max_batch) fail(SMX_ECONFIG, "CNN: n_val must be a multiple of max_batch");
             c->cnn = true;
@@ -825,7 +825,6 @@ int smx_open(const smx_model_desc* desc, int device, int n_slots, int n_ckpts, s
             c->al = cnn::act_layout(d.max_batch);
             c->act_stride = c->al.stride;
             c->d_in = cnn::kSample;
-            c->lockstep_launches = d.gemm_mode == SMX_GEMM_TC ? 18 : 13;
         }
         try {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
@@ -1224,7 +1223,7 @@ int smx_train(smx_ctx* c, int n_active, const int* slots, int n_steps) {
             smx_ctx::Graph& g = graph_for(c, v);
             for (int i = 0; i < n_steps; ++i) {
                 ck(cudaGraphLaunch(g.exec, c->stream), "graph launch");
-                c->stats.launches += c->lockstep_launches;
+                c->stats.launches += g.launches;
             }
         } else {
             ck(cudaMemcpyAsync(c->scratch_slots, v.data(), sizeof(int) * n_active, cudaMemcpyHostToDevice, c->stream),
