@@ -446,8 +446,12 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             char* bl = bh + nt * 128;
             if constexpr (Op::B_IMAGE) {
                 if (gt == 0) {  // the weight image of this chunk: one bulk copy of hi | lo
+#ifdef SMX_DBG_NO_BIMG  // profiling variant: no weight-image copies (B = whatever the stage holds)
+                    mbar_arrive(&full[s]);
+#else
                     mbar_arrive_expect_tx(&full[s], nt * 256);
                     bulk_g2s(bh, op.b_image(c), nt * 256, &full[s]);
+#endif
                 }
             }
             // A hi/lo -> TMEM (lane = row, column = k)
