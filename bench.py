@@ -33,15 +33,18 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-# DRAM bytes (read + write) per launch of each candidate roofline kernel (64 groups at bs 128)
-# from one `ncu --set full` capture of a 64-slot lockstep (profiles/r02/ncu_convs_v14.txt)
+# DRAM bytes (read + write) per launch of each candidate roofline kernel (64 groups at bs 128,
+# max_batch 128) from one `ncu --set full` capture of a 64-slot lockstep
+# (profiles/r02/ncu_convs_v15.txt, profiles/debug/r2s3_ncu_all.sh)
 TRAFFIC: dict = {
-    "K1_conv2_fwd": 1_083_998_000 + 539_703_000,
-    "K3_conv2_wgrad": 1_613_875_000 + 70_186_000,
-    "K2_conv2_dgrad": 587_868_000 + 1_017_241_000,
-    "K2_conv3_dgrad": 349_032_000 + 487_305_000,
-    "K1_conv3_fwd": 576_542_000 + 254_631_000,
-    "K3_conv3_wgrad": 838_719_000 + 71_447_000,
+    "K1_conv2_fwd": 1_084_283_000 + 542_001_000,
+    "K3_conv2_wgrad": 1_613_928_000 + 70_167_000,
+    "K2_conv2_dgrad": 587_626_000 + 1_015_939_000,
+    "K2_conv3_dgrad": 346_514_000 + 487_264_000,
+    "K1_conv3_fwd": 575_331_000 + 28_835_000,
+    "K3_conv3_wgrad": 845_850_000 + 70_262_000,
+    "K1_conv1_fwd": 13_078_000 + 1_014_505_000,
+    "K3_conv1_wgrad": 1_083_643_000 + 11_760_000,
 }
 # what each candidate is (tensor-core mode, per launch = 64 groups at bs 128)
 KERNEL_DESC: dict = {
@@ -456,8 +459,8 @@ def main():
             "K3_conv3_wgrad": tensor("wgrad3", gemm_flops, ms[7]),
             # conv1 (tensor cores, HBM-bound): the forward writes a1 (128 x 1024 x 32 fp32 per slot)
             # and reads the images (128 x 4096 fp32); the weight gradient reads dA1 and the images
-            "K1_conv1_fwd": hbm("fwd1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[9]),
-            "K3_conv1_wgrad": hbm("wgrad1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[8]),
+            "K1_conv1_fwd": hbm("fwd1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[9], traffic=TRAFFIC["K1_conv1_fwd"]),
+            "K3_conv1_wgrad": hbm("wgrad1", n_k * 128 * (1024 * 32 + 4096) * 4, ms[8], traffic=TRAFFIC["K3_conv1_wgrad"]),
             "K5_update": hbm("upd", upd_bytes, ms[0], slots=n_h),
             "K6_fork": hbm("fork", fork_bytes, ms[1], checkpoints=n_h),
         }

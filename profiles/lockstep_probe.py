@@ -19,9 +19,10 @@ ap.add_argument("--bs", type=int, default=128)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--model", default="mlp", choices=["mlp", "cnn"])
+ap.add_argument("--max-batch", type=int, default=0, help="0: the executor default")
 a = ap.parse_args()
 e = ex.Executor(n_slots=a.slots, n_ckpts=4, max_steps=64, gemm_mode=ex.GEMM_TC if a.gemm == "tc" else ex.GEMM_EXACT,
-                model=ex.MODEL_CNN if a.model == "cnn" else ex.MODEL_MLP)
+                model=ex.MODEL_CNN if a.model == "cnn" else ex.MODEL_MLP, **({"max_batch": a.max_batch} if a.max_batch else {}))
 e.set_graphs(False)
 hp = np.tile(np.float32([0.05, 0.9, 1e-4, a.bs]), (64, 1))
 for s in range(a.slots):
