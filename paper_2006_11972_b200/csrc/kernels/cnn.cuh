@@ -434,22 +434,36 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
         for (int k = 0; k < kNC; ++k) dzs[k] = dzo[k] = __fdiv_rn(dz[k], fb);
         for (int k = kNC; k < kNCP; ++k) dzs[k] = dzo[k] = 0.0f;
     }
-    __syncthreads();
     // the pool / ReLU backward of this sample (formerly head_dg_kernel, same arithmetic):
     // dg[c] = (fmaf chain over k < 16 of dz * W4[k][c]) * 2^-6; d3[n][p][c] = (a3 > 0) ? dg[c] : 0
+    __shared__ float dgs[kFeat];
+    __shared__ uint32_t mks[64 * (kFeat / 32)];
+    const uint32_t* mk = reinterpret_cast<const uint32_t*>(v.act + p.al.mk3) + (long long)n * 64 * (kFeat / 32);
+    if (p.pooled)  // a3 > 0 as the bitmap the conv3 forward epilogue wrote: word (n, pix, c / 32), staged coalesced
+        for (int i = c; i < 64 * (kFeat / 32); i += 128) mks[i] = __ldg(mk + i);
+    __syncthreads();
     float acc = 0.0f;
 #pragma unroll
     for (int k = 0; k < kNCP; ++k) acc = __fmaf_rn(dzs[k], v.w[kOffW4 + k * kFeat + c], acc);
-    const float dg = __fmul_rn(acc, 0.015625f);
-    float* d3 = v.act + p.al.d3 + (long long)n * 64 * kFeat;
-    if (p.pooled) {  // a3 > 0 as the bitmap the conv3 forward epilogue wrote: word (n, pix, c / 32)
-        const uint32_t* mk = reinterpret_cast<const uint32_t*>(v.act + p.al.mk3) + (long long)n * 64 * (kFeat / 32) + c / 32;
-#pragma unroll 16
-        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = (__ldg(mk + pix * (kFeat / 32)) >> (c & 31)) & 1u ? dg : 0.0f;
-    } else {
-        const float* a3 = v.act + p.al.a3 + (long long)n * 64 * kFeat;
-#pragma unroll 16
-        for (int pix = 0; pix < 64; ++pix) d3[pix * kFeat + c] = __ldg(a3 + pix * kFeat + c) > 0.0f ? dg : 0.0f;
+    dgs[c] = __fmul_rn(acc, 0.015625f);
+    __syncthreads();
+    // thread = 4 channels (cq) x 16 pixels (pg): 16-byte stores, a warp writes 512 contiguous bytes
+    const int cq = c & 31, pg = c >> 5;
+    const float4 dg4 = reinterpret_cast<const float4*>(dgs)[cq];
+    float4* d3 = reinterpret_cast<float4*>(v.act + p.al.d3 + (long long)n * 64 * kFeat) + cq;
+    const float4* a3 = reinterpret_cast<const float4*>(v.act + p.al.a3 + (long long)n * 64 * kFeat) + cq;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+        const int pix = pg * 16 + i;
+        bool m0, m1, m2, m3;
+        if (p.pooled) {
+            const uint32_t w = mks[pix * (kFeat / 32) + (cq >> 3)] >> ((cq & 7) * 4);
+            m0 = w & 1u; m1 = (w >> 1) & 1u; m2 = (w >> 2) & 1u; m3 = (w >> 3) & 1u;
+        } else {
+            const float4 a = __ldg(a3 + pix * (kFeat / 4));
+            m0 = a.x > 0.0f; m1 = a.y > 0.0f; m2 = a.z > 0.0f; m3 = a.w > 0.0f;
+        }
+        d3[pix * (kFeat / 4)] = make_float4(m0 ? dg4.x : 0.0f, m1 ? dg4.y : 0.0f, m2 ? dg4.z : 0.0f, m3 ? dg4.w : 0.0f);
     }
 }
 
