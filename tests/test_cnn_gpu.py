@@ -90,9 +90,12 @@ def rel(a, b):
     return np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30)
 
 
-def test_tc_first_step_gradient(ds):
+@pytest.mark.parametrize("bs", [1, 5, 16, 37, 64])
+def test_tc_first_step_gradient(ds, bs):
+    # bs 1 / 5 / 37: batch sizes that are not multiples of the conv1 weight-gradient work item
+    # (4 samples) and of the 8 image-row chunks, and batches smaller than one item
     _, _, off = ol.cnn_layout()
-    for bs in (16, 64):
+    if True:
         hp = np.tile(np.float32([1.0, 0.0, 0.0, bs]), (4, 1))   # m_1 = gradient
         with make(ex.GEMM_TC) as e:
             e.slot_init(0)
@@ -114,12 +117,16 @@ def test_tc_first_step_gradient(ds):
         # evaluation orders (measured: conv1 channel 14 at bs 16 flips for TC, at bs 64 for the
         # oracle itself), which moves that output channel's gradient by ~1e-3 relative.  The
         # bound is therefore per output channel: 90% of channels within 2e-5, every tensor 2e-3.
+        # Small batches (bs 5) leave fp32 itself above 2e-5 on the conv1 bias (a 5 x 1024-term sum
+        # with cancellation): the per-channel bound is 2e-5 or twice the fp32 oracle's own error.
         cout = (32, 32, 64, 64, 128, 128, 16, 16)
         for i, (a, b) in enumerate(zip(off[:8], off[1:9])):
             assert rel(m[a:b], g64[a:b]) <= 2e-3, (bs, i, rel(m[a:b], g64[a:b]))
             rows = [r for r in np.split(np.arange(a, b), cout[i]) if np.linalg.norm(g64[r]) > 0]
             errs = sorted(rel(m[r], g64[r]) for r in rows)
-            assert errs[int(0.9 * (len(errs) - 1))] <= 2e-5, (bs, i, errs[-3:])
+            oerrs = sorted(rel(o.m[r], g64[r]) for r in rows)
+            bound = max(2e-5, 2 * oerrs[int(0.9 * (len(oerrs) - 1))])
+            assert errs[int(0.9 * (len(errs) - 1))] <= bound, (bs, i, errs[-3:], bound)
 
 
 def test_tc_trajectory_and_eval_within_tolerance(ds):
