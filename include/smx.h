@@ -163,6 +163,11 @@ int smx_reset_stats(smx_ctx* ctx);
  * 8 = the conv1 weight gradient (with its reduction), 9 = the conv1 forward.
  * Returns mean CUDA-event ms per launch. */
 int smx_bench_kernel(smx_ctx* ctx, int kind, int n, int reps, double* ms_per_launch);
+/* K7 measurement: n <= 16 checkpoint entries 0..n-1 of `src` copied to entries 0..n-1 of `dst` per
+ * launch (the fork kernel on dst reading src's pool through peer loads; a staged runtime peer copy
+ * without P2P access), `reps` launches timed with CUDA events on dst's stream.  Returns mean ms
+ * per entry copied. */
+int smx_bench_peer_copy(smx_ctx* dst, smx_ctx* src, int n, int reps, double* ms_per_copy);
 
 /* Test hook: one ungrouped GEMM C[M x N] = A op B on the device through the executor's GEMM
  * kernels (gemm_mode of the context): am/bm = 0 when A(m,k) = A[m*lda+k] / B(n,k) = B[n*ldb+k],

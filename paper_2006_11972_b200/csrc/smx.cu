@@ -1121,6 +1121,57 @@ int smx_ckpt_peer_copy(smx_ctx* dst, int dst_ckpt, smx_ctx* src, int src_ckpt) {
     });
 }
 
+int smx_bench_peer_copy(smx_ctx* dst, smx_ctx* src, int n, int reps, double* ms_per_copy) {
+    return guard([&] {
+        if (n < 1 || n > 16 || n > dst->C || n > src->C || reps < 1) fail(SMX_ECONFIG, "bench_peer_copy: 1 <= n <= 16");
+        if (dst->palloc != src->palloc) fail(SMX_ECONFIG, "peer copy between different models");
+        for (int i = 0; i < n; ++i)
+            if (!src->ck_valid[i]) fail(SMX_EINTEGRITY, "peer copy from empty checkpoint entry");
+        cudaSetDevice(src->device);
+        ck(cudaStreamSynchronize(src->stream), "src sync");
+        cudaSetDevice(dst->device);
+        bool direct = dst->device == src->device;
+        if (!direct) {
+            int can = 0;
+            ck(cudaDeviceCanAccessPeer(&can, dst->device, src->device), "can access peer");
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer");
+                cudaGetLastError();
+                direct = true;
+            }
+        }
+        // K7 as the engine issues it, n entries per launch (the fork kernel reading the source
+        // pool through peer loads), reps launches between events on the destination stream
+        CopyBatch<16> b{};
+        for (int i = 0; i < n; ++i)
+            b.j[i] = CopyJob{reinterpret_cast<const float4*>(src->pool + src->slab_stride() * i),
+                             reinterpret_cast<float4*>(dst->pool + dst->slab_stride() * i), src->ck_st + i, dst->ck_st + i};
+        const long long n4 = 2 * dst->palloc / 4;
+        const size_t bytes = sizeof(float) * dst->slab_stride();
+        auto once = [&] {
+            if (direct) {
+                fork_copy_kernel<16><<<dim3(fork_blocks(n4), n), 256, 0, dst->stream>>>(b, n4);
+                launch_check(dst, "bench peer fork_copy");
+            } else {
+                for (int i = 0; i < n; ++i)
+                    ck(cudaMemcpyPeerAsync(dst->pool + dst->slab_stride() * i, dst->device, src->pool + src->slab_stride() * i,
+                                           src->device, bytes, dst->stream),
+                       "peer copy");
+            }
+        };
+        once();
+        cudaEventRecord(dst->ev[6], dst->stream);
+        for (int r = 0; r < reps; ++r) once();
+        cudaEventRecord(dst->ev[7], dst->stream);
+        ck(cudaEventSynchronize(dst->ev[7]), "bench sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, dst->ev[6], dst->ev[7]);
+        *ms_per_copy = (double)ms / ((double)reps * n);
+        for (int i = 0; i < n; ++i) dst->ck_valid[i] = 1;
+    });
+}
+
 int smx_slot_state(smx_ctx* c, int slot, int64_t* step, int64_t* offset) {
     return guard([&] {
         check_slot(c, slot);

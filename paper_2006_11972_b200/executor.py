@@ -29,7 +29,8 @@ EXPORTS = (
     "smx_host_free", "smx_hp_upload", "smx_slot_init",
     "smx_slot_load", "smx_slot_save", "smx_release_slot", "smx_ckpt_free", "smx_ckpt_peer_copy", "smx_slot_state", "smx_slot_read",
     "smx_slot_write", "smx_ckpt_read", "smx_ckpt_write", "smx_train", "smx_eval", "smx_losses", "smx_sync",
-    "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel", "smx_test_gemm",
+    "smx_set_timing", "smx_set_graphs", "smx_get_stats", "smx_reset_stats", "smx_bench_kernel", "smx_bench_peer_copy",
+    "smx_test_gemm",
     "smx_last_error", "smx_version",
 )
 
@@ -107,6 +108,7 @@ def load_library() -> ctypes.CDLL:
             "smx_get_stats": [P, ctypes.POINTER(Stats)],
             "smx_reset_stats": [P],
             "smx_bench_kernel": [P, I, I, I, ctypes.POINTER(ctypes.c_double)],
+            "smx_bench_peer_copy": [P, P, I, I, ctypes.POINTER(ctypes.c_double)],
             "smx_test_gemm": [P, I, I, I, I, I, FP, I, FP, I, FP],
         }
         for name, args in sig.items():
@@ -292,6 +294,12 @@ class Executor:
         _check(self._lib.smx_test_gemm(self._ctx, int(a_mn), int(b_mn), M, N, K, _fp(A), A.shape[1], _fp(B),
                                        B.shape[1], _fp(C)))
         return C
+
+    def bench_peer_copy(self, src: "Executor", n: int, reps: int) -> float:
+        """Mean ms per checkpoint entry copied from `src` (K7, n entries per launch)."""
+        out = ctypes.c_double()
+        _check(self._lib.smx_bench_peer_copy(self._ctx, src._ctx, n, reps, ctypes.byref(out)))
+        return out.value
 
     def bench_kernel(self, kind: int, n: int, reps: int) -> float:
         out = ctypes.c_double()

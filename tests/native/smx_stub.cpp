@@ -262,6 +262,7 @@ int smx_reset_stats(smx_ctx* c) {
     return SMX_OK;
 }
 int smx_bench_kernel(smx_ctx*, int, int, int, double*) { return err(SMX_ECONFIG, "stub has no kernels"); }
+int smx_bench_peer_copy(smx_ctx*, smx_ctx*, int, int, double*) { return err(SMX_ECONFIG, "stub has no kernels"); }
 int smx_test_gemm(smx_ctx*, int, int, int, int, int, const float*, int, const float*, int, float*) {
     return err(SMX_ECONFIG, "stub has no kernels");
 }
