@@ -914,218 +914,9 @@ __global__ void __launch_bounds__(256) weight_image_kernel(ConvArgs p) {
         weight_image_body<3>(p, b - kWImgBlocks1 - kWImgBlocks2, kWImgBlocks3);
 }
 
-// ---- layer 1 in tensor-core mode: fp32 SIMT kernels ---------------------------------------
-// conv1 has K = 27 and N = 32: far too thin for 128-row tcgen05 tiles.  These kernels use fp32
-// FMAs (at least as accurate as 3xTF32) in their own fixed order, issued as packed FFMA2 (two
-// output channels per instruction: the 3-register FFMA issues at half rate on this part, so the
-// packed form is what reaches the FMA pipe's throughput); exact mode keeps the oracle-order
-// kernels above.
-
-// Packed fp32 FMA (FFMA2): a register pair of accumulators += a register pair x a scalar that
-// ptxas broadcasts to both halves (written here as the pair {x, x}).
-__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ float2 f2unpack(unsigned long long v) {
-    float2 r;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-    return r;
-}
-
-// conv1 forward: block = one (sample, slot); thread = an output-channel pair (co, co + 1) x 8
-// consecutive pixels of a row, the pair's 27 weights held as packed register pairs so every
-// packed FMA (FFMA2) computes both channels from one broadcast input value.  The sample's
-// zero-padded image is staged in shared memory as channel planes [3][34][36]; a half-warp (16
-// channel pairs) shares each plane segment it loads (10 values per row of taps and channel, two
-// LDS.128 + one LDS.64), so shared-memory traffic is ~1 byte per 5 FMAs.  A warp walks 4 output
-// rows, 16 pixels (two 8-pixel halves, one per half-warp) per iteration; each pixel's 32 channels
-// leave as one 128-byte segment (8-byte stores of the channel pairs).  A block walks samples
-// x, x + gridDim.x, ... of its slot, loading the next image while computing the current one.
-// grid (min(max_batch, 32), groups), block 256.
-constexpr int kPlW = 36, kPlane = 34 * kPlW;
-__global__ void __launch_bounds__(256) conv1_fwd_lane(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
-    if ((int)blockIdx.x >= v.bs) return;
-    __shared__ __align__(16) float pl[3 * kPlane];
-    for (int i = threadIdx.x; i < 3 * kPlane; i += blockDim.x) pl[i] = 0.0f;  // borders stay zero
-    const float* in = layer_in<1>(p, v);
-    // samples blockIdx.x, + gridDim.x, ...: the next sample's image is loaded into registers
-    // while the current one is computed
-    float4 img[4];
-    auto load = [&](int n) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            img[j] = __ldg(reinterpret_cast<const float4*>(in + (long long)n * 4096 + (threadIdx.x + 256 * j) * 4));
-    };
-    auto stage = [&]() {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int i = threadIdx.x + 256 * j;
-            const int o = ((i >> 5) + 1) * kPlW + (i & 31) + 1;  // padded (row, column)
-            pl[o] = img[j].x; pl[kPlane + o] = img[j].y; pl[2 * kPlane + o] = img[j].z;
-        }
-    };
-    load(blockIdx.x);
-    __syncthreads();
-    stage();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cp = lane & 15, half = lane >> 4, co = 2 * cp;
-    unsigned long long w[27];  // (W[co][t][ci], W[co + 1][t][ci])
-#pragma unroll
-    for (int t = 0; t < 9; ++t)
-#pragma unroll
-        for (int ci = 0; ci < 3; ++ci)
-            w[t * 3 + ci] = f2pack(__ldg(v.w + Geo<1>::OffW + (co * 9 + t) * 4 + ci),
-                                   __ldg(v.w + Geo<1>::OffW + ((co + 1) * 9 + t) * 4 + ci));
-    const unsigned long long bias = f2pack(__ldg(v.w + Geo<1>::OffB + co), __ldg(v.w + Geo<1>::OffB + co + 1));
-    __syncthreads();
-#pragma unroll 1
-    for (int n = blockIdx.x; n < v.bs; n += gridDim.x) {
-        const bool more = n + (int)gridDim.x < v.bs;
-        if (more) load(n + gridDim.x);
-        float* out = layer_out<1>(p, v) + (long long)n * 1024 * 32 + co;
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {  // 4 rows x 2 sixteen-pixel halves per warp
-            const int oh = warp * 4 + (q >> 1), p0 = (q & 1) * 16 + half * 8;
-            unsigned long long acc[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] = bias;
-#pragma unroll
-            for (int dh = 0; dh < 3; ++dh)
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci) {
-                    // padded columns p0 .. p0 + 9 of row oh + dh, channel ci
-                    const float* r = pl + ci * kPlane + (oh + dh) * kPlW + p0;
-                    const float4 x0 = *reinterpret_cast<const float4*>(r);
-                    const float4 x1 = *reinterpret_cast<const float4*>(r + 4);
-                    const float2 x2 = *reinterpret_cast<const float2*>(r + 8);
-                    const float x[10] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y};
-#pragma unroll
-                    for (int dw = 0; dw < 3; ++dw) {
-                        const unsigned long long wt = w[(dh * 3 + dw) * 3 + ci];
-#pragma unroll
-                        for (int px = 0; px < 8; ++px)
-                            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[px]) : "l"(wt), "l"(f2pack(x[px + dw], x[px + dw])));
-                    }
-                }
-#pragma unroll
-            for (int px = 0; px < 8; ++px) {
-                const float2 r = f2unpack(acc[px]);
-                *reinterpret_cast<float2*>(out + (oh * 32 + p0 + px) * 32) =
-                    make_float2(fmaxf(r.x, 0.0f), fmaxf(r.y, 0.0f));
-            }
-        }
-        if (more) {
-            __syncthreads();  // every warp is done with this sample's planes
-            stage();
-            __syncthreads();
-        }
-    }
-}
-
-// Per-sample partial weight gradient of conv1 with packed FMAs, the forward's structure with the
-// roles of weights and pixels swapped: thread = output-channel pair (co, co + 1) x one 8-pixel
-// segment per step; its 27 (tap, ci) accumulators (+ bias) are register pairs, and each FFMA2
-// adds the pair's two output gradients (one 8-byte load, 128 bytes per half-warp and pixel) times
-// a broadcast input value read from the planar image.  The next segment's output gradients are
-// loaded while the current one is accumulated; the 16 segment streams of a block are combined in
-// a fixed order per sample.  A block walks samples x, x + gridDim.x, ... of its slot with the next
-// image prefetched.  partial[n][co*28 + j], j = tap*3 + ci (27 = bias).  grid (min(max_batch, 32),
-// groups), block 256.
-__global__ void __launch_bounds__(256, 2) conv1_wgrad_lane(ConvArgs p) {
-    const SlotView v = slot_view(p, p.slots[blockIdx.y]);
-    if ((int)blockIdx.x >= v.bs) return;
-    __shared__ __align__(16) float pl[3 * kPlane];
-    __shared__ float red[8][kL1Outs];
-    for (int i = threadIdx.x; i < 3 * kPlane; i += blockDim.x) pl[i] = 0.0f;  // borders stay zero
-    const float* in = layer_in<1>(p, v);
-    float4 img[4];
-    auto load = [&](int n) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            img[j] = __ldg(reinterpret_cast<const float4*>(in + (long long)n * 4096 + (threadIdx.x + 256 * j) * 4));
-    };
-    auto stage = [&]() {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int i = threadIdx.x + 256 * j;
-            const int o = ((i >> 5) + 1) * kPlW + (i & 31) + 1;
-            pl[o] = img[j].x; pl[kPlane + o] = img[j].y; pl[2 * kPlane + o] = img[j].z;
-        }
-    };
-    load(blockIdx.x);
-    __syncthreads();
-    stage();
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cp = lane & 15, half = lane >> 4, co = 2 * cp;
-    const unsigned long long one = f2pack(1.0f, 1.0f);
-#pragma unroll 1
-    for (int n = blockIdx.x; n < v.bs; n += gridDim.x) {
-        const bool more = n + (int)gridDim.x < v.bs;
-        if (more) load(n + gridDim.x);
-        const float* dy = layer_dout<1>(p, v) + (long long)n * 1024 * 32 + co;
-        auto seg_px = [&](int q) { return (warp * 4 + (q >> 1)) * 32 + (q & 1) * 16 + half * 8; };
-        unsigned long long acc[28];
-#pragma unroll
-        for (int j = 0; j < 28; ++j) acc[j] = 0ull;
-        unsigned long long d[8], dn[8];
-#pragma unroll
-        for (int px = 0; px < 8; ++px) d[px] = __ldg(reinterpret_cast<const unsigned long long*>(dy + (seg_px(0) + px) * 32));
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {
-            const int m0 = seg_px(q), oh = m0 >> 5, p0 = m0 & 31;
-            if (q + 1 < 8) {
-                const int m1 = seg_px(q + 1);
-#pragma unroll
-                for (int px = 0; px < 8; ++px) dn[px] = __ldg(reinterpret_cast<const unsigned long long*>(dy + (m1 + px) * 32));
-            }
-#pragma unroll
-            for (int dh = 0; dh < 3; ++dh)
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci) {
-                    const float* r = pl + ci * kPlane + (oh + dh) * kPlW + p0;
-                    const float4 x0 = *reinterpret_cast<const float4*>(r);
-                    const float4 x1 = *reinterpret_cast<const float4*>(r + 4);
-                    const float2 x2 = *reinterpret_cast<const float2*>(r + 8);
-                    const float x[10] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y};
-#pragma unroll
-                    for (int dw = 0; dw < 3; ++dw)
-#pragma unroll
-                        for (int px = 0; px < 8; ++px)
-                            asm("fma.rn.f32x2 %0, %1, %2, %0;"
-                                : "+l"(acc[(dh * 3 + dw) * 3 + ci]) : "l"(d[px]), "l"(f2pack(x[px + dw], x[px + dw])));
-                }
-#pragma unroll
-            for (int px = 0; px < 8; ++px) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[27]) : "l"(d[px]), "l"(one));
-#pragma unroll
-            for (int px = 0; px < 8; ++px) d[px] = dn[px];
-        }
-        // half-warps hold the same channel pair: fold, then the 8 warps in order
-#pragma unroll
-        for (int j = 0; j < 28; ++j) {
-            float2 a = f2unpack(acc[j]);
-            a.x = __fadd_rn(a.x, __shfl_xor_sync(0xffffffffu, a.x, 16));
-            a.y = __fadd_rn(a.y, __shfl_xor_sync(0xffffffffu, a.y, 16));
-            if (half == 0) {
-                red[warp][co * 28 + j] = a.x;
-                red[warp][(co + 1) * 28 + j] = a.y;
-            }
-        }
-        __syncthreads();
-        float* part = v.act + p.al.w1p + (long long)n * kL1Outs;
-        for (int i = threadIdx.x; i < kL1Outs; i += blockDim.x) {
-            float s_ = red[0][i];
-#pragma unroll
-            for (int w = 1; w < 8; ++w) s_ = __fadd_rn(s_, red[w][i]);
-            part[i] = s_;
-        }
-        if (more) stage();
-        __syncthreads();  // planes and red reused by the next sample
-    }
-}
+// ---- layer 1 in tensor-core mode: the tcgen05 kernels are in conv1_tc.cuh (round 1 ran conv1 on
+// packed-FFMA2 CUDA-core kernels: FMA-pipe bound at 57-66 %, 331 + 434 us per 64-slot lockstep
+// against 193 + 288 us now; profiles/r02/SUMMARY.md).  The partial rows they write are summed here.
 
 // Sum the partial rows (one per `per_part` consecutive samples) in order into the gradient slab,
 // or (fuse_update) apply K5 to the parameter in place.  grid (7, groups), block 128.

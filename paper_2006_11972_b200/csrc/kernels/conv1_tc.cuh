@@ -2,7 +2,7 @@
 // N = 32, far too thin for a 128-row tile in its natural im2col form; both kernels here reshape it.
 //
 // ---------------------------------------------------------------------------------------------
-// Weight gradient (replaces the FFMA2 kernel conv1_wgrad_lane, FMA-pipe bound at ~57 %):
+// Weight gradient (round 1 ran it on a packed-FFMA2 CUDA-core kernel, FMA-pipe bound at ~57 %):
 //
 //   dW1[co][kh][kw][ci] = sum_{n, h, w} dA1[n][h][w][co] * X[n][h + kh - 1][w + kw - 1][ci]
 //
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1_wgrad_tc_kernel(ConvArgs p,
 }
 
 // ---------------------------------------------------------------------------------------------
-// conv1 forward on the tensor cores (tensor-core mode; replaces the FFMA2 kernel conv1_fwd_lane,
+// conv1 forward on the tensor cores (tensor-core mode; round 1 used a packed-FFMA2 kernel,
 // FMA-pipe bound at ~66 %).  An HBM-bound implicit GEMM: a 128-pixel tile (4 image rows of 32) =
 // M, N = 32 output channels, K = 9 taps x 4 channels (the fourth is the zero pad) + 4 zeros = 40,
 // 5 k-steps; the weight operand is the pre-split hi / lo image of weight_image_kernel<1> (K-major

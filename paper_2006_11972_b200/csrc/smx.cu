@@ -387,13 +387,7 @@ template <int L>
 void conv_forward(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        static const bool lane_kernel = std::getenv("SMX_CONV1_FWD_LANE") != nullptr;  // A/B: the FFMA2 kernel
-        if (lane_kernel) {
-            cnn::conv1_fwd_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
-            launch_check(c, "conv1_fwd_lane");
-        } else {
-            conv1_fwd_tc(c, a, mb, n);
-        }
+        conv1_fwd_tc(c, a, mb, n);
         return;
     }
     if (c->d.gemm_mode == SMX_GEMM_TC) {
@@ -409,14 +403,8 @@ template <int L>
 void conv_wgrad(smx_ctx* c, const cnn::ConvArgs& a, int n, int mb) {
     using G = cnn::Geo<L>;
     if (c->d.gemm_mode == SMX_GEMM_TC && L == 1) {
-        static const bool lane_kernel = std::getenv("SMX_CONV1_WGRAD_LANE") != nullptr;  // A/B: the FFMA2 kernel
-        if (lane_kernel) {
-            cnn::conv1_wgrad_lane<<<dim3(std::min(mb, 32), n), 256, 0, c->cur>>>(a);
-            launch_check(c, "conv1_wgrad_lane");
-        } else {
-            conv1_wgrad_tc(c, a, mb, n);
-        }
-        cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a, lane_kernel ? 1 : cnn::c1::kImgs);
+        conv1_wgrad_tc(c, a, mb, n);
+        cnn::conv1_wgrad_reduce<<<dim3((cnn::kL1Outs + 127) / 128, n), 128, 0, c->cur>>>(a, cnn::c1::kImgs);
         launch_check(c, "conv1_wgrad_reduce");
         return;
     }
