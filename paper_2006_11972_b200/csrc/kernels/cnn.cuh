@@ -520,10 +520,12 @@ struct Fwd {
     static constexpr bool A_TMA = (L >= 2);  // A tile = one strided TMA box per chunk
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_SEG_CHUNKS, kEpiWarps = L == 3 ? 8 : 4;
     static constexpr int kRowsPerSample = G::OH * G::OH;
-    // the producers also record the ReLU mask of the layer input (conv2: a1, conv3: a2) as a bitmap
-    // for the input gradient of this layer: the taps (kh, kw) in {1, 2}^2 of a stride-2 conv visit
-    // every input pixel exactly once, and a producer thread holds 32 consecutive channels of it
-    static constexpr bool kInMaskBits = (L >= 2), kMaskFromBits = false, kSgd = false;
+    // the ReLU masks the input gradients read are bitmaps: a1's is written by the conv1 forward
+    // epilogue, a3's by the pooled conv3 epilogue, and a2's by the conv3 forward producers (the taps
+    // (kh, kw) in {1, 2}^2 of a stride-2 conv visit every input pixel exactly once, and a producer
+    // thread holds 32 consecutive channels of it).  (The conv2 forward epilogue writing a2's bits
+    // instead made that 4-warp epilogue the kernel's bottleneck: 470 -> 620 us.)
+    static constexpr bool kInMaskBits = (L == 3), kMaskFromBits = false, kSgd = false;
     // conv3: the epilogue pools each sample's 64 output pixels into g (the head's input, in
     // head_fwd's order) and writes the a3 > 0 bitmap for head_dg instead of storing a3 itself
     static constexpr bool kPool = (L == 3);

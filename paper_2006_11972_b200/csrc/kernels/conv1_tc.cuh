@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1_wgrad_tc_kernel(ConvArgs p,
 //   warp 9      MMA: 5 k-steps x (A_hi W_hi, A_hi W_lo [, A_lo W_hi]) into one of two accumulators
 //   warps 4-7   epilogue (quadrant q): + bias, ReLU, the pixel's 32 channels (128 B) into a
 //               per-warp 128-byte-swizzled staging tile (conflict-free), one 4 KB TMA tensor store
-//               per warp and tile row (kTmA1)
+//               per warp and tile row (kTmA1), and the pixel's a1 > 0 bitmap word (mk1)
 // Items (slot, sample) are split into contiguous per-CTA ranges (a CTA stays on one slot, so the
 // weight image is reloaded only when the slot changes).
 namespace f1 {
@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_fwd_tc_kernel(ConvArgs p, i
 #pragma unroll
             for (int c = 0; c < 32; ++c) bias[c] = __ldg(v.w + Geo<1>::OffB + c);
             const CUtensorMap* omap = p.tmaps + (long long)slot * kTmapKinds + kTmA1;
+            uint32_t* mk1 = reinterpret_cast<uint32_t*>(v.act + p.al.mk1);
             for (int tr = 0; tr < 8; ++tr, ++t) {
                 const int a = t & 1;
                 mbar_wait(&accf[a], (t >> 1) & 1);
@@ -548,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_fwd_tc_kernel(ConvArgs p, i
                 // 128-byte swizzle (16-byte chunk c of row p at c ^ (p % 8)): conflict-free stores,
                 // and the layout the TMA store un-swizzles
                 float4* row = reinterpret_cast<float4*>(stg + a * 1024 + lane * 32);
+                uint32_t bits = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int c4 = i;
@@ -557,7 +559,11 @@ __global__ void __launch_bounds__(kThreads, 2) conv1_fwd_tc_kernel(ConvArgs p, i
                     o.z = fmaxf(__fadd_rn(__uint_as_float(r[4 * c4 + 2]), bias[4 * c4 + 2]), 0.0f);
                     o.w = fmaxf(__fadd_rn(__uint_as_float(r[4 * c4 + 3]), bias[4 * c4 + 3]), 0.0f);
                     row[c4 ^ (lane & 7)] = o;
+                    bits |= ((o.x > 0.0f ? 1u : 0u) | (o.y > 0.0f ? 2u : 0u) | (o.z > 0.0f ? 4u : 0u) |
+                             (o.w > 0.0f ? 8u : 0u)) << (4 * c4);
                 }
+                // the pixel's a1 > 0 bitmap word (the conv2 input gradient's ReLU mask)
+                mk1[(long long)n * 1024 + (tr * 4 + q) * 32 + lane] = bits;
                 asm volatile("fence.proxy.async.shared::cta;");
                 __syncwarp();
 #ifdef F1_DBG_NO_STORE
