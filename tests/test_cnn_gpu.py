@@ -90,43 +90,62 @@ def rel(a, b):
     return np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30)
 
 
+def check_first_step(ds, bs, maxb=MAXB, chan_bound=2e-5):
+    """One tensor-core step at batch size bs (mu = 0: m_1 = the gradient) against the fp32 oracle's
+    loss and a float64 torch gradient."""
+    _, _, off = ol.cnn_layout()
+    hp = np.tile(np.float32([1.0, 0.0, 0.0, bs]), (4, 1))
+    with ex.Executor(n_slots=4, n_ckpts=2, gemm_mode=ex.GEMM_TC, max_steps=64, max_batch=maxb, n_train=N_TRAIN,
+                     n_val=N_VAL, model=ex.MODEL_CNN) as e:
+        e.slot_init(0)
+        e.hp_upload(0, 0, hp)
+        e.train([0], 1)
+        _, m = e.slot_read(0)
+        loss = e.losses(0, 0, 1)[0]
+    o = ol.CnnSlot(ds, max_steps=4)
+    w0 = o.w.copy()
+    o.train(hp, 1)
+    assert abs(loss - o.loss[0]) <= 2e-6 * abs(o.loss[0])
+    # float64 ground truth: long reductions (up to bs x 1024 terms with cancellation) make the
+    # fp32 oracle itself ~1e-4 off for conv1; the TC path must be as good as fp32 is
+    params = unpack(w0)
+    tl, _ = torch_loss(params, ds.x[:bs], ds.y[:bs])
+    tl.backward()
+    g64 = grad_vector(params, w0)
+    # A pre-activation within ~1e-7 of 0 can flip its ReLU mask between any two fp32 evaluation
+    # orders (measured: conv1 channel 14 at bs 16 flips for TC, at bs 64 for the oracle itself),
+    # which moves that output channel's gradient by ~1e-3 relative.  The bound is therefore per
+    # output channel: 90% of channels within 2e-5 (or twice the fp32 oracle's own error where that
+    # is larger), every tensor within 2e-3.
+    cout = (32, 32, 64, 64, 128, 128, 16, 16)
+    for i, (a, b) in enumerate(zip(off[:8], off[1:9])):
+        assert rel(m[a:b], g64[a:b]) <= 2e-3, (bs, i, rel(m[a:b], g64[a:b]))
+        rows = [r for r in np.split(np.arange(a, b), cout[i]) if np.linalg.norm(g64[r]) > 0]
+        errs = sorted(rel(m[r], g64[r]) for r in rows)
+        oerrs = sorted(rel(o.m[r], g64[r]) for r in rows)
+        bound = max(chan_bound, 2 * oerrs[int(0.9 * (len(oerrs) - 1))])
+        assert errs[int(0.9 * (len(errs) - 1))] <= bound, (bs, i, errs[-3:], bound)
+
+
 @pytest.mark.parametrize("bs", [1, 5, 16, 37, 64])
 def test_tc_first_step_gradient(ds, bs):
     # bs 1 / 5 / 37: batch sizes that are not multiples of the conv1 weight-gradient work item
     # (4 samples) and of the 8 image-row chunks, and batches smaller than one item
-    _, _, off = ol.cnn_layout()
-    if True:
-        hp = np.tile(np.float32([1.0, 0.0, 0.0, bs]), (4, 1))   # m_1 = gradient
-        with make(ex.GEMM_TC) as e:
-            e.slot_init(0)
-            e.hp_upload(0, 0, hp)
-            e.train([0], 1)
-            _, m = e.slot_read(0)
-            loss = e.losses(0, 0, 1)[0]
-        o = ol.CnnSlot(ds, max_steps=4)
-        w0 = o.w.copy()
-        o.train(hp, 1)
-        assert abs(loss - o.loss[0]) <= 2e-6 * abs(o.loss[0])
-        # float64 ground truth: long reductions (up to bs x 1024 terms with cancellation) make the
-        # fp32 oracle itself ~1e-4 off for conv1; the TC path must be as good as fp32 is
-        params = unpack(w0)
-        tl, _ = torch_loss(params, ds.x[:bs], ds.y[:bs])
-        tl.backward()
-        g64 = grad_vector(params, w0)
-        # A pre-activation within ~1e-7 of 0 can flip its ReLU mask between any two fp32
-        # evaluation orders (measured: conv1 channel 14 at bs 16 flips for TC, at bs 64 for the
-        # oracle itself), which moves that output channel's gradient by ~1e-3 relative.  The
-        # bound is therefore per output channel: 90% of channels within 2e-5, every tensor 2e-3.
-        # Small batches (bs 5) leave fp32 itself above 2e-5 on the conv1 bias (a 5 x 1024-term sum
-        # with cancellation): the per-channel bound is 2e-5 or twice the fp32 oracle's own error.
-        cout = (32, 32, 64, 64, 128, 128, 16, 16)
-        for i, (a, b) in enumerate(zip(off[:8], off[1:9])):
-            assert rel(m[a:b], g64[a:b]) <= 2e-3, (bs, i, rel(m[a:b], g64[a:b]))
-            rows = [r for r in np.split(np.arange(a, b), cout[i]) if np.linalg.norm(g64[r]) > 0]
-            errs = sorted(rel(m[r], g64[r]) for r in rows)
-            oerrs = sorted(rel(o.m[r], g64[r]) for r in rows)
-            bound = max(2e-5, 2 * oerrs[int(0.9 * (len(oerrs) - 1))])
-            assert errs[int(0.9 * (len(errs) - 1))] <= bound, (bs, i, errs[-3:], bound)
+    check_first_step(ds, bs)
+
+
+@pytest.mark.parametrize("bs", [200, 256])
+def test_tc_first_step_gradient_max_batch_256(bs):
+    # The largest batch (C3's bs 256 step): 8 weight-gradient splits of 2,048 rows for conv2, a
+    # partial last split at bs 200, 64 conv1 work items per slot.  At this size the weight
+    # gradients of conv1 / conv2 (bs x 1024 / bs x 256 terms per weight) are dominated by ReLU-mask
+    # flips of their input activations: pre-activations within the forward's rounding of 0 change
+    # mask between any two fp32 orders, and their number grows with bs.  Measured 90th-percentile
+    # channel errors vs float64 at bs 200 / 256: fp32 oracle 2-6e-6, tensor-core path 2.9-4.2e-5
+    # (segmenting the conv1 forward's TMEM accumulation 5 ways did not change this, swapping its
+    # tcgen05 forward for fp32 FMA chains halved it).  Per-channel bound here: 1e-4 (tf32 alone
+    # would be ~1e-3); every tensor still within 2e-3.
+    check_first_step(ol.cnn_dataset(N_TRAIN, N_VAL, 256), bs, maxb=256, chan_bound=1e-4)
 
 
 def test_tc_trajectory_and_eval_within_tolerance(ds):
