@@ -417,7 +417,25 @@ __global__ void __launch_bounds__(128) head_fwd_kernel(ConvArgs p) {
         if (!p.zout) v.act[p.al.g + (long long)n * kFeat + c] = g[c];
     }
     __syncthreads();
-    if (c < kNCP) {
+    if (p.pooled) {
+        // tensor-core mode: warp w computes z[4w .. 4w + 3], lane = 4 strided channels, then a
+        // fixed shuffle tree (instead of one 128-long fmaf chain per output: the head is latency-bound)
+        const int lane = c & 31, w = c >> 5;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const int k = 4 * w + kk;
+            const float* wr = v.w + kOffW4 + k * kFeat;
+            float acc = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc = __fmaf_rn(g[lane + 32 * j], __ldg(wr + lane + 32 * j), acc);
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+            if (lane == 0) {
+                z[k] = __fadd_rn(acc, v.w[kOffB4 + k]);
+                if (p.zout) p.zout[p.z_stride * blockIdx.y + ((long long)p.x_row0 + n) * kNCP + k] = z[k];
+            }
+        }
+    } else if (c < kNCP) {  // exact mode: the oracle's chain
         const float* wr = v.w + kOffW4 + c * kFeat;
         float acc = 0.0f;
         for (int i = 0; i < kFeat; ++i) acc = __fmaf_rn(g[i], wr[i], acc);
