@@ -42,6 +42,18 @@ constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K
 constexpr int kARawTile = kBM * kKC * 4;         // raw A tile, 16 KB: [128 rows][32 k] (16-B units
                                                  // XOR-swizzled by row) or [32 k][128 rows]
 
+// Ops with kTmaOut (the conv2 input gradient): the epilogue sums a tile's segments in registers
+// (thread = row x 64 columns), stages the masked tile in the segment-sum area in the layout of one
+// TMA box (Op::stage_out) and writes it with one tensor store (Op::store_tile)
+template <class Op, class = void>
+struct TmaOut {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct TmaOut<Op, std::void_t<decltype(Op::kTmaOut)>> {
+    static constexpr bool value = Op::kTmaOut;
+};
+
 // Shared-memory plan of one Op, sized by its N (the B tiles and the segment sums scale with it):
 // kStages B stages | kARaw raw A tiles | barriers | segment sums.  The raw-A ring takes what is
 // left of the 227 KB (at most 8 deep): the prefetch distance is kARaw - 1 chunks.
@@ -53,8 +65,8 @@ struct WsPlan {
     static constexpr int Sacc = kBM * N * 4;                        // tile sums [row][N], 16-B units
                                                                     // XOR-swizzled by row
     // masked epilogues reading the ReLU mask as a bitmap stage the tile's words in shared memory
-    static constexpr int MaskWords = (Op::EPI == 1 && Op::kMaskFromBits) ? kBM * N / 32 : 0;
-    static constexpr int BarBytes = 512;
+    static constexpr int MaskWords = (Op::EPI == 1 && Op::kMaskFromBits && !TmaOut<Op>::value) ? kBM * N / 32 : 0;
+    static constexpr int BarBytes = TmaOut<Op>::value ? 1024 : 512;  // (a staged TMA box starts 1 KB-aligned)
     static constexpr int Fixed = Stages * BStage + BarBytes + Sacc + MaskWords * 4;
     static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
     // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
@@ -65,6 +77,7 @@ struct WsPlan {
     static constexpr int SaccOff = BarOff + BarBytes;
     static constexpr int MbitsOff = SaccOff + Sacc;
     static constexpr int Bytes = MbitsOff + MaskWords * 4;
+    static_assert(!TmaOut<Op>::value || SaccOff % 1024 == 0, "staging box alignment");
     // epilogue: one warp per TMEM lane quadrant (4), or two each draining half the columns (8)
     static constexpr int EpiWarps = Op::kEpiWarps;
     static_assert(EpiWarps == 4 || EpiWarps == 8, "epilogue warps");
@@ -661,9 +674,71 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         // (register sums only where the register budget allows: the 13-warp kernels)
         constexpr bool kRegSum = Plan::EpiWarps == 4 && kCW <= 64 && kCW % 16 == 0;
         static_assert(!(kRegSum && ColRanges<Op>::value), "column ranges need the shared-memory segment sums");
+        // TmaOut: which 32-column class blocks each segment writes (bit = block; its first chunk's
+        // range, all blocks for the first segment) and the last segment writing each block
+        uint32_t seg_cols = 0, last_seg = 0;  // 4 bits per segment (<= 8) / per block
+        if constexpr (TmaOut<Op>::value) {
+            static_assert(Plan::N == 128, "4 class blocks");
+            for (int j = 0; j < nseg && j < 8; ++j) {
+                int slo = 0, sn = nt;
+                if constexpr (ColRanges<Op>::value)
+                    if (j > 0) op.chunk_cols(op.kbeg + j * seg * kKC, slo, sn);
+                for (int bb = 0; bb < 4; ++bb)
+                    if (32 * bb < slo + sn && 32 * bb + 32 > slo) {
+                        seg_cols |= 1u << (4 * j + bb);
+                        last_seg = (last_seg & ~(15u << (4 * bb))) | ((uint32_t)j << (4 * bb));
+                    }
+            }
+        }
         int un = 0;
         for (int i = 0; i < ntiles; ++i) {
             const int mt0 = (tile0 + i) * kBM;
+            if constexpr (TmaOut<Op>::value) {
+                // ---- segments summed straight into the staged output box, one TMA store per tile
+                static_assert(Plan::EpiWarps == 8 && Plan::N == 128, "TMA-out epilogue mapping");
+                const int m = mt0 + row;
+                uint32_t mw[2];
+#pragma unroll
+                for (int cb = 0; cb < 2; ++cb) mw[cb] = m < M ? op.mask_word(m, cbeg + 32 * cb) : 0u;
+                char* stg = smem + Plan::SaccOff;
+                // the previous tile's store has finished reading the staging area
+                if (et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");
+                for (int j = 0; j < nseg; ++j, ++un) {
+                    const int acc_i = un & 1, use = un >> 1;
+                    SMX_TL(2048 + un * 4 + 0, et == 0);
+                    mbar_wait(&accf[acc_i], use & 1);
+                    SMX_TL(2048 + un * 4 + 1, et == 0);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+                    for (int cb = 0; cb < 2; ++cb) {
+                        if (!((seg_cols >> (4 * j + 2 * ch + cb)) & 1u)) continue;
+                        const int c0 = cbeg + 32 * cb;
+                        const bool last = ((last_seg >> (4 * (2 * ch + cb))) & 15u) == (uint32_t)j;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t r[16];
+                            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc_i * kAcc + c0 + 16 * h, r);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#ifndef SMX_DBG_NO_EPI
+                            op.stage16(stg, row, c0 + 16 * h, r, j == 0, last, cb ? mw[1] : mw[0]);
+#endif
+                        }
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&acce[acc_i]);
+                }
+                SMX_TL(3072 + i * 2 + 0, et == 0);
+                asm volatile("fence.proxy.async.shared::cta;");  // generic stores -> the TMA's async proxy
+                asm volatile("bar.sync 2, %0;" ::"n"(Plan::EpiThreads) : "memory");
+#ifndef SMX_DBG_NO_EPI
+                if (et == 0) {
+                    op.store_tile(smem_u32(stg), tile0 + i);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+#endif
+                SMX_TL(3072 + i * 2 + 1, et == 0);
+            } else {
             // bitmap masks: the tile's words are loaded now (in flight during the drains) and staged
             // in shared memory before the scatter
             constexpr int kMW = Plan::MaskWords > 0 ? Plan::MaskWords / Plan::EpiThreads : 1;
@@ -954,7 +1029,10 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 SMX_TL(3072 + i * 2 + 1, et == 0);
             }
 #endif
+            }  // !TmaOut
         }
+        if constexpr (TmaOut<Op>::value)
+            if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the last tile's store
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();

@@ -268,6 +268,19 @@ void make_conv_tmaps(smx_ctx* c) {
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (a1) failed (" + std::to_string((int)r) + ")");
     }
+    // the conv2 input gradient's output d1 as {32 channels, 32 columns, max_batch x 32 rows}: one
+    // box = the 16 input rows of one M tile (64 KB)
+    for (int s = 0; s < c->S; ++s) {
+        float* base = c->act + c->act_stride * s + c->al.d1;
+        const cuuint64_t dims[3] = {32, 32, (cuuint64_t)(mb * 32)};
+        const cuuint64_t strides[2] = {32 * 4, 32 * 32 * 4};
+        const cuuint32_t box[3] = {32, 32, 16};
+        const cuuint32_t es[3] = {1, 1, 1};
+        const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + cnn::kTmD1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (d1) failed (" + std::to_string((int)r) + ")");
+    }
     ck(cudaMalloc(&c->tmaps, sizeof(CUtensorMap) * h.size()), "tensor maps");
     ck(cudaMemcpy(c->tmaps, h.data(), sizeof(CUtensorMap) * h.size(), cudaMemcpyHostToDevice), "tensor maps H2D");
 }
