@@ -151,7 +151,7 @@ inline ActLayout act_layout(int max_batch) {
 // stride of 2), the conv2 / conv3 output gradients (d2 / d3) of the sub-pixel input gradients, and
 // the weight gradients' im2col operands (a1 / a2 again, one box of 32 output pixels x all input
 // channels per tap).
-enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmWgB2 = 6, kTmWgB3 = 7, kTmA1 = 8, kTmD1 = 9, kTmapKinds = 10 };
+enum { kTmFwd2 = 0, kTmFwd3 = 1, kTmDgr2 = 2, kTmDgr3 = 3, kTmWg2 = 4, kTmWg3 = 5, kTmWgB2 = 6, kTmWgB3 = 7, kTmA1 = 8, kTmD1 = 9, kTmD2 = 10, kTmapKinds = 11 };
 // kTmWgB2 / kTmWgB3: the weight gradients' B operand (the layer's output gradient d2 / d3 as a
 // 2-D [sample x pixel][Co] tensor): 32 x 32 boxes with the 128-byte / 32-byte-atom swizzle = the
 // UMMA MN-major tf32 layout (SWIZZLE_128B_BASE32B), loaded straight into the B stage.
@@ -658,10 +658,11 @@ struct Dgrad {
     static constexpr bool kInMaskBits = false, kMaskFromBits = true, kSgd = false;
     static constexpr int kOnesRow = -1, kPartLd = 0, kSegChunks = SMX_DGR_SEG_CHUNKS, kEpiWarps = 8;
     static constexpr int HH = G::H / 2;  // == OH
-    // conv2: the tile's output (16 input rows x 32 columns x 32 channels of one sample, 64 KB
-    // contiguous in d1) is staged in shared memory in the 128B-swizzled layout of the kTmD1 box
-    // and written by one TMA tensor store (conv_ws TmaOut)
-    static constexpr bool kTmaOut = (L == 2);
+    // The tile's output is staged in shared memory in the 128B-swizzled layout of TMA boxes and
+    // written by tensor stores (conv_ws TmaOut): conv2 = 16 input rows x 32 columns x 32 channels
+    // of one sample (64 KB contiguous in d1, one kTmD1 box); conv3 = the N tile's parity row pi of
+    // 2 samples (8 rows x 16 columns x 64 channels each), two kTmD2 boxes of 32 channels
+    static constexpr bool kTmaOut = true;
     // Column position -> parity class.  conv2 orders its 4 classes 0, 1, 3, 2 so that the classes
     // fed by each output neighbour (da, db) -- those with (pi or !da) and (pj or !db) -- are
     // contiguous: (0,0) all, (0,1) {1, 3}, (1,0) {3, 2}, (1,1) {3}; the MMAs of a K chunk then
@@ -701,7 +702,7 @@ struct Dgrad {
         const SlotView v = slot_view(p, p.slots[z]);
         dy = layer_dout<L>(p, v);
         tmap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 2 ? kTmDgr2 : kTmDgr3);
-        omap = p.tmaps + (long long)v.slot * kTmapKinds + kTmD1;
+        omap = p.tmaps + (long long)v.slot * kTmapKinds + (L == 2 ? kTmD1 : kTmD2);
         w = v.w + G::OffW;
         mbits = reinterpret_cast<const uint32_t*>(v.act + (L == 2 ? p.al.mk1 : p.al.mk2));
         dx = layer_dout<L - 1>(p, v);
@@ -761,24 +762,31 @@ struct Dgrad {
     __device__ __forceinline__ void store_masked(int, int, long long off, float4 x) const {
         __stcs(reinterpret_cast<float4*>(dx + off), x);  // streaming: read next by another kernel
     }
-    // kTmaOut staging of tile row `row` (= (a, b) within the tile), 16 columns [col, col + 16) (4
-    // channel quads of one class), r = their values of one accumulation segment: the first segment
-    // writes them, later ones add (round-to-nearest), and the segment that completes the columns
-    // applies the ReLU mask (word mw: the pixel's 32 channel bits).  Box line L = (2 a + pi) x 32 +
-    // 2 b + pj holds the 32 channels of one input pixel; 16-byte unit u sits at u ^ (L & 7)
-    // (SWIZZLE_128B).  Lanes b and b + 4 would share units, so lanes with bit 2 of b set take the
-    // units of each pair in the order u ^ 1: every 8 lanes then cover the 8 units of a bank row
-    // (4 wavefronts per warp store).
+    // kTmaOut staging of tile row `row`, 16 columns [col, col + 16) (4 channel quads of one class),
+    // r = their values of one accumulation segment: the first segment writes them, later ones add
+    // (round-to-nearest), and the segment that completes the columns applies the ReLU mask (word
+    // mw: the pixel's 32 channel bits of these columns).  A box line (128 bytes) holds 32 channels
+    // of one input pixel; conv2: line (2 a + pi) x 32 + 2 b + pj, conv3: box ci / 32, line
+    // (sample x 8 + a) x 16 + 2 b + pj.  16-byte unit u sits at u ^ (line & 7) (SWIZZLE_128B).
+    // Lanes b and b + 4 would share units, so lanes with bit 2 of b set take the units of each pair
+    // in the order u ^ 1: every 8 lanes then cover the 8 units of a bank row (4 wavefronts per
+    // warp store).
     __device__ __forceinline__ void stage16(char* stg, int row, int col, const uint32_t* r, bool first, bool last,
                                             uint32_t mw) const {
-        static_assert(L == 2, "TMA output staging is laid out for conv2");
-        const int al = row >> 4, b = row & 15, rot = (b >> 2) & 1;
-        const int cls = cls_at(col >> 5), pi = cls >> 1, pj = cls & 1;
-        const int Ln = (2 * al + pi) * 32 + 2 * b + pj;
-        char* line = stg + Ln * 128;
+        const int b = row % HH, rot = (b >> 2) & 1;
+        const int cls = cls_at((col0 + col) / G::Ci), pi = cls >> 1, pj = cls & 1, ci = (col0 + col) % G::Ci;
+        int Ln;
+        char* box = stg;
+        if constexpr (L == 2) {
+            Ln = (2 * (row / HH) + pi) * 32 + 2 * b + pj;
+        } else {
+            Ln = ((row / (HH * HH)) * HH + (row / HH) % HH) * 16 + 2 * b + pj;
+            box += (ci >> 5) * 32768;
+        }
+        char* line = box + Ln * 128;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int u = (((col & 31) >> 2) + j) ^ rot;  // channel quad written by this step
+            const int u = (((ci & 31) >> 2) + j) ^ rot;  // channel quad written by this step
             float4 v;
             v.x = __uint_as_float(rot ? r[4 * (j ^ 1)] : r[4 * j]);
             v.y = __uint_as_float(rot ? r[4 * (j ^ 1) + 1] : r[4 * j + 1]);
@@ -802,13 +810,26 @@ struct Dgrad {
             *dst = v;
         }
     }
-    // the staged tile -> d1 rows 2 a0 .. 2 a0 + 15 of its sample (kTmD1: {32 channels, 32 columns,
-    // max_batch x 32 rows}, box {32, 32, 16})
+    // the staged tile -> dx.  conv2: d1 rows 2 a0 .. 2 a0 + 15 of its sample (kTmD1: {32 channels,
+    // 32 columns, max_batch x 32 rows}, box {32, 32, 16}).  conv3: d2 as {64 channels, 16 columns,
+    // 2 row parities, 8 row pairs, max_batch} (kTmD2), boxes {32, 16, 1, 8, 2} at channels 0 / 32,
+    // parity pi of this N tile, samples 2 tile, 2 tile + 1 (a partial last tile writes zeros into
+    // sample bs < max_batch, which the step never reads, or is clipped at max_batch)
     __device__ __forceinline__ void store_tile(uint32_t stg, int tile) const {
-        const int m0 = tile * kBM, n = m0 / (HH * HH), a0 = (m0 % (HH * HH)) / HH;
-        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(omap),
-                     "r"(0), "r"(0), "r"(n * G::H + 2 * a0), "r"(stg)
-                     : "memory");
+        if constexpr (L == 2) {
+            const int m0 = tile * kBM, n = m0 / (HH * HH), a0 = (m0 % (HH * HH)) / HH;
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(omap),
+                         "r"(0), "r"(0), "r"(n * G::H + 2 * a0), "r"(stg)
+                         : "memory");
+        } else {
+            const int pi = cls_at(col0 / G::Ci) >> 1;
+#pragma unroll
+            for (int bx = 0; bx < 2; ++bx)
+                asm volatile(
+                    "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(omap),
+                    "r"(32 * bx), "r"(0), "r"(pi), "r"(0), "r"(2 * tile), "r"(stg + bx * 32768)
+                    : "memory");
+        }
     }
 };
 

@@ -42,9 +42,10 @@ constexpr int kBTile = kKQ * 128 * 16;           // B hi (or lo) tile, compact K
 constexpr int kARawTile = kBM * kKC * 4;         // raw A tile, 16 KB: [128 rows][32 k] (16-B units
                                                  // XOR-swizzled by row) or [32 k][128 rows]
 
-// Ops with kTmaOut (the conv2 input gradient): the epilogue sums a tile's segments in registers
-// (thread = row x 64 columns), stages the masked tile in the segment-sum area in the layout of one
-// TMA box (Op::stage_out) and writes it with one tensor store (Op::store_tile)
+// Ops with kTmaOut (the input gradients): the epilogue adds a tile's segments straight into the
+// segment-sum area laid out as the tile's TMA output boxes (Op::stage16; thread = row x 64
+// columns), the segment completing a column masks it, and tensor stores write the tile
+// (Op::store_tile)
 template <class Op, class = void>
 struct TmaOut {
     static constexpr bool value = false;

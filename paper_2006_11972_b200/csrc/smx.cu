@@ -281,6 +281,19 @@ void make_conv_tmaps(smx_ctx* c) {
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (d1) failed (" + std::to_string((int)r) + ")");
     }
+    // the conv3 input gradient's output d2 as {64 channels, 16 columns, 2 row parities, 8 row
+    // pairs, max_batch}: one box = 32 channels of one parity row set of two samples (32 KB)
+    for (int s = 0; s < c->S; ++s) {
+        float* base = c->act + c->act_stride * s + c->al.d2;
+        const cuuint64_t dims[5] = {64, 16, 2, 8, (cuuint64_t)mb};
+        const cuuint64_t strides[4] = {64 * 4, 16 * 64 * 4, 2 * 16 * 64 * 4, 16 * 16 * 64 * 4};
+        const cuuint32_t box[5] = {32, 16, 1, 8, 2};
+        const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        const CUresult r = enc(&h[(size_t)s * cnn::kTmapKinds + cnn::kTmD2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, base,
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(SMX_EDEVICE, "cuTensorMapEncodeTiled (d2) failed (" + std::to_string((int)r) + ")");
+    }
     ck(cudaMalloc(&c->tmaps, sizeof(CUtensorMap) * h.size()), "tensor maps");
     ck(cudaMemcpy(c->tmaps, h.data(), sizeof(CUtensorMap) * h.size(), cudaMemcpyHostToDevice), "tensor maps H2D");
 }
