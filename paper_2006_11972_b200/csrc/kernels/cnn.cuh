@@ -663,6 +663,29 @@ struct Dgrad {
     // of one sample (64 KB contiguous in d1, one kTmD1 box); conv3 = the N tile's parity row pi of
     // 2 samples (8 rows x 16 columns x 64 channels each), two kTmD2 boxes of 32 channels
     static constexpr bool kTmaOut = true;
+    // conv2: chunk c = output neighbour c % 4 x channels 32 (c / 4) ..; the 4 neighbours' A tiles
+    // are windows of one TMA box of dy (the tile's 8 output rows + 1 x 16 columns + 1, zero
+    // filled past the image: 9 x 17 pixels x 32 channels) read from one raw slot (conv_ws ANbrBox).
+    // The reduction order changes with it: a 4-chunk accumulation segment = one 32-channel group
+    // over all neighbours.
+    static constexpr bool kANbrBox = (L == 2);
+    static constexpr int kABoxBytes = 32 * 17 * 9 * 4;
+    __host__ __device__ static constexpr int chunk_k0(int c) {
+        return L == 2 ? (c & 3) * G::Co + (c >> 2) * 32 : c * 32;
+    }
+    // line (pixel) of the neighbour box holding row r's A values for chunk c
+    __device__ __forceinline__ int a_line(int r, int c) const {
+        const int nb = c & 3;
+        return ((r / HH) + (nb >> 1)) * 17 + (r % HH) + (nb & 1);
+    }
+    // neighbour box origin (channel, column, row, sample) of tile `tile`, channel group cu
+    __device__ __forceinline__ void a_box(int tile, int cu, int* c) const {
+        const int m0 = tile * kBM;
+        c[0] = cu * 32;
+        c[1] = 0;
+        c[2] = (m0 % (HH * HH)) / HH;
+        c[3] = m0 / (HH * HH);
+    }
     // Column position -> parity class.  conv2 orders its 4 classes 0, 1, 3, 2 so that the classes
     // fed by each output neighbour (da, db) -- those with (pi or !da) and (pj or !db) -- are
     // contiguous: (0,0) all, (0,1) {1, 3}, (1,0) {3, 2}, (1,1) {3}; the MMAs of a K chunk then
@@ -974,7 +997,7 @@ __device__ __forceinline__ void weight_image_body(const ConvArgs& p, int bx, int
             const int pi = cls >> 1, pj = cls & 1;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int k = c * 32 + kq * 4 + e;
+                const int k = ctc::Dgrad<(L >= 2 ? L : 2)>::chunk_k0(c) + kq * 4 + e;
                 const int nb = k / G::Co, co = k % G::Co, da = nb >> 1, db = nb & 1;
                 const int kh = pi ? (da ? 0 : 2) : (da ? -1 : 1);
                 const int kw = pj ? (db ? 0 : 2) : (db ? -1 : 1);

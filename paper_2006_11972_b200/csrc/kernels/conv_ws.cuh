@@ -55,6 +55,26 @@ struct TmaOut<Op, std::void_t<decltype(Op::kTmaOut)>> {
     static constexpr bool value = Op::kTmaOut;
 };
 
+// Ops with kANbrBox (the conv2 input gradient): chunk c of a tile reads output neighbour c % 4 of
+// channels 32 (c / 4) ..; one TMA box (Op::kABoxBytes: the tile's rows + one row and column of
+// neighbours) feeds those 4 chunks from one raw slot (Op::a_line(row, c) = the row's 128-byte
+// line), released by the 8 producer warps after their last chunk of it.  Op::chunk_k0(c) is the
+// chunk's reduction offset.
+template <class Op, class = void>
+struct ANbrBox {
+    static constexpr bool value = false;
+    static constexpr int bytes = 0;
+};
+template <class Op>
+struct ANbrBox<Op, std::void_t<decltype(Op::kANbrBox)>> {
+    static constexpr bool value = Op::kANbrBox;
+    static constexpr int bytes = Op::kABoxBytes;
+};
+template <class Op>
+__device__ __forceinline__ int chunk_k0(const Op& op, int c) {
+    if constexpr (ANbrBox<Op>::value) return op.kbeg + Op::chunk_k0(c); else return op.kbeg + c * kKC;
+}
+
 // Shared-memory plan of one Op, sized by its N (the B tiles and the segment sums scale with it):
 // kStages B stages | kARaw raw A tiles | barriers | segment sums.  The raw-A ring takes what is
 // left of the 227 KB (at most 8 deep): the prefetch distance is kARaw - 1 chunks.
@@ -69,12 +89,14 @@ struct WsPlan {
     static constexpr int MaskWords = (Op::EPI == 1 && Op::kMaskFromBits && !TmaOut<Op>::value) ? kBM * N / 32 : 0;
     static constexpr int BarBytes = TmaOut<Op>::value ? 1024 : 512;  // (a staged TMA box starts 1 KB-aligned)
     static constexpr int Fixed = Stages * BStage + BarBytes + Sacc + MaskWords * 4;
-    static constexpr int ARawMax = (227 * 1024 - Fixed) / kARawTile;
+    // raw A slot: one chunk's tile, or (ANbrBox) one neighbour box of 4 chunks (1 KB-aligned)
+    static constexpr int ARawTile = ANbrBox<Op>::value ? (ANbrBox<Op>::bytes + 1023) / 1024 * 1024 : kARawTile;
+    static constexpr int ARawMax = (227 * 1024 - Fixed) / ARawTile;
     // two producer groups take alternate chunks; each prefetches ARaw/2 - 1 of its own chunks
-    static constexpr int ARaw = (ARawMax > 8 ? 8 : ARawMax) & ~1;
-    static_assert(ARaw >= 4, "shared memory plan");
+    static constexpr int ARaw = ANbrBox<Op>::value ? (ARawMax > 8 ? 8 : ARawMax) : (ARawMax > 8 ? 8 : ARawMax) & ~1;
+    static_assert(ARaw >= (ANbrBox<Op>::value ? 2 : 4), "shared memory plan");
     static constexpr int ARawOff = Stages * BStage;
-    static constexpr int BarOff = ARawOff + ARaw * kARawTile;
+    static constexpr int BarOff = ARawOff + ARaw * ARawTile;
     static constexpr int SaccOff = BarOff + BarBytes;
     static constexpr int MbitsOff = SaccOff + Sacc;
     static constexpr int Bytes = MbitsOff + MaskWords * 4;
@@ -254,7 +276,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
         if constexpr (Op::A_TMA)
             for (int r = 0; r < kARaw; ++r) {
                 mbar_init(&rawf[r], 1);
-                mbar_init(&rawe[r], 4);
+                mbar_init(&rawe[r], ANbrBox<Op>::value ? 8 : 4);
             }
         if constexpr (Op::B_TMA)
             for (int st = 0; st < kStages; ++st) mbar_init(&bfull[st], 1);
@@ -360,7 +382,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             const int s = g % kStages, u = g / kStages;
             SMX_TL(g * 8 + 0, gt == 0);
             const int m = (tile0 + i) * kBM + q * 32 + lane;
-            const int k0 = op.kbeg + c * kKC;
+            const int k0 = chunk_k0(op, c);
             // B (register path, non-image Ops): the group's 128 threads cover the tile
             float4 b[8];
 #ifdef SMX_DBG_NO_BREG
@@ -402,7 +424,11 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                 }
             }
             float a[32];
-            if constexpr (Op::A_TMA)
+            // raw slot of this chunk (neighbour boxes: one per 4 chunks)
+            const int a_slot = ANbrBox<Op>::value ? (g >> 2) % kARaw : rd_slot;
+            if constexpr (ANbrBox<Op>::value)
+                mbar_wait(&rawf[a_slot], ((g >> 2) / kARaw) & 1);
+            else if constexpr (Op::A_TMA)
                 mbar_wait(&rawf[rd_slot], ((((g - grp) >> 1) / (kARaw / 2)) & 1));
             else if constexpr (kDw > 1)
                 asm volatile("cp.async.wait_group %0;" ::"n"(kDw - 1) : "memory");  // own copies of chunk g
@@ -411,9 +437,17 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             __syncwarp();
             SMX_TL(g * 8 + 1, gt == 0);
             {
-                const char* rawg = smem + Plan::ARawOff + rd_slot * kARawTile;
+                const char* rawg = smem + Plan::ARawOff + a_slot * Plan::ARawTile;
                 const int r = q * 32 + lane;
-                if constexpr (Op::AM == 0) {
+                if constexpr (ANbrBox<Op>::value) {
+                    // the row's line of the neighbour box (128B-swizzled by line)
+                    const int ln = op.a_line(r, c);
+#pragma unroll
+                    for (int kq = 0; kq < 8; ++kq) {
+                        const float4 t = *reinterpret_cast<const float4*>(rawg + ln * 128 + ((kq ^ (ln & 7)) << 4));
+                        a[4 * kq] = t.x; a[4 * kq + 1] = t.y; a[4 * kq + 2] = t.z; a[4 * kq + 3] = t.w;
+                    }
+                } else if constexpr (Op::AM == 0) {
 #pragma unroll
                     for (int kq = 0; kq < 8; ++kq) {
                         const float4 t = *reinterpret_cast<const float4*>(rawg + r * 128 + ((kq ^ (r & 7)) << 4));
@@ -435,7 +469,6 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             // (TMA operands: the slot is released only once the loaded registers have been
             // consumed by the TMEM stores below; an arrive right after the LDS instructions could
             // overtake loads still in flight, and the TMA warp would refill the slot under them)
-            const int a_slot = rd_slot;
             SMX_TL(g * 8 + 5, gt == 0);
             a_issue();
             rd_slot += 2;
@@ -514,7 +547,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             SMX_TL(g * 8 + 4, gt == 0);
             if constexpr (Op::A_TMA) {
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&rawe[a_slot]);
+                if (lane == 0 && (!ANbrBox<Op>::value || (g & 3) >= 2)) mbar_arrive(&rawe[a_slot]);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;");
             asm volatile("fence.proxy.async.shared::cta;");
@@ -533,6 +566,24 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             if (lane == 0) {
                 constexpr int kBoxBytes = kARawTile / Op::kBoxes;
                 const uint32_t araw = smem_u32(smem + Plan::ARawOff);
+                if constexpr (ANbrBox<Op>::value) {
+                    // one neighbour box per 4 chunks of a tile
+                    const int per_tile = nchunks / 4;
+                    for (int u = 0; u < total / 4; ++u) {
+                        const int slot = u % kARaw, use = u / kARaw;
+                        if (use > 0) mbar_wait(&rawe[slot], (use - 1) & 1);
+                        const uint32_t bar = smem_u32(&rawf[slot]), dst = araw + slot * Plan::ARawTile;
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                                     "r"(ANbrBox<Op>::bytes));
+                        int cc[4];
+                        op.a_box(tile0 + u / per_tile, u % per_tile, cc);
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+                            "l"(op.tmap), "r"(cc[0]), "r"(cc[1]), "r"(cc[2]), "r"(cc[3]), "r"(bar)
+                            : "memory");
+                    }
+                } else {
                 int tile = 0, c = 0;
                 for (int g = 0; g < total; ++g) {
                     const int slot = g % kARaw, use = g / kARaw;
@@ -551,6 +602,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                             : "memory");
                     }
                     if (++c == nchunks) { c = 0; ++tile; }
+                }
                 }
             }
             __syncwarp();
@@ -606,10 +658,10 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t bhi = smem_base + s * kBStage, blo = bhi + nt * 128;
                     const uint32_t ahi = tmem + kABase + s * 64, alo = ahi + 32;
-                    const int ksteps = (min(kKC, klim - (op.kbeg + c * kKC)) + 7) / 8;
+                    const int ksteps = (min(kKC, klim - chunk_k0(op, c)) + 7) / 8;
                     // accumulator columns of this chunk (all of them unless the Op skips zero blocks)
                     int coff = 0, cn = nt;
-                    if constexpr (ColRanges<Op>::value) op.chunk_cols(op.kbeg + c * kKC, coff, cn);
+                    if constexpr (ColRanges<Op>::value) op.chunk_cols(chunk_k0(op, c), coff, cn);
                     const uint32_t idc = ColRanges<Op>::value ? idesc_tf32(cn) | (Op::B_TMA ? (1u << 16) : 0u) : idesc;
                     const uint32_t dac = dacc + coff;
                     // descriptors built once per chunk; a k-step of 8 tf32 advances the B tiles by
@@ -683,7 +735,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
             for (int j = 0; j < nseg && j < 8; ++j) {
                 int slo = 0, sn = nt;
                 if constexpr (ColRanges<Op>::value)
-                    if (j > 0) op.chunk_cols(op.kbeg + j * seg * kKC, slo, sn);
+                    if (j > 0) op.chunk_cols(chunk_k0(op, j * seg), slo, sn);
                 for (int bb = 0; bb < 4; ++bb)
                     if (32 * bb < slo + sn && 32 * bb + 32 > slo) {
                         seg_cols |= 1u << (4 * j + bb);
@@ -829,7 +881,7 @@ __global__ void __launch_bounds__(WsPlan<Op>::Threads, 1) conv_ws_kernel(typenam
                     int slo = 0, shi = nt;
                     if constexpr (ColRanges<Op>::value) {
                         int sn;
-                        op.chunk_cols(op.kbeg + j * seg * kKC, slo, sn);
+                        op.chunk_cols(chunk_k0(op, j * seg), slo, sn);
                         shi = slo + sn;
                     }
                     // 32 columns per TMEM round trip (two loads in flight before one wait)

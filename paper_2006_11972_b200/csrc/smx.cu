@@ -216,7 +216,7 @@ void make_conv_tmaps(smx_ctx* c) {
     const Spec specs[cnn::kTmWgB2] = {
         {c->al.a1, 32, 32, 32, 1, 16, 8, 2},   // conv2 forward: a1, output tile = 8 rows x 16 columns
         {c->al.a2, 64, 16, 16, 2, 8, 8, 2},    // conv3 forward: a2, 2 samples x 8 x 8
-        {c->al.d2, 64, 16, 16, 1, 16, 8, 1},   // conv2 input gradient: d2, 8 x 16 blocks
+        {c->al.d2, 64, 16, 16, 1, 17, 9, 1},   // conv2 input gradient: d2, 8 x 16 blocks + their (1, 1) neighbours
         {c->al.d3, 128, 8, 8, 2, 8, 8, 1},     // conv3 input gradient: d3, 2 samples x 8 x 8 blocks
         {c->al.a1, 32, 32, 32, 1, 33, 5, 1},   // conv2 weight gradient: a1 window of 32 output pixels (2 x 16), all taps
         {c->al.a2, 64, 16, 16, 1, 8, 4, 2},    // conv3 weight gradient: a2, 32 output pixels (4 x 8) per tap
