@@ -340,11 +340,21 @@ constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 8; }
 template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
     configure_ws<Op>(c);
-    // tiles per CTA: as many as the Op likes (fewer pipeline fills) while the grid still gives
-    // every SM at least two CTAs; it changes only the work split, never the arithmetic
+    // tiles per CTA (one CTA per SM at a time): the count <= the Op's maximum that minimises
+    // waves x (tiles + per-CTA fill / drain ~0.6 tile), so that the last wave is not a short one
+    // at any slot count (e.g. 10 slots of the conv2 input gradient: 8 tiles per CTA = 2.2 waves,
+    // 6 = 2.9).  It changes only the work split, never the arithmetic.
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
-    int tpc = conv_tpc<Op>();
-    while (tpc > 1 && (long long)gx * ((mtiles + tpc - 1) / tpc) * groups < 2 * 148) tpc /= 2;
+    int tpc = 1;
+    double best = 1e30;
+    for (int t = conv_tpc<Op>(); t >= 1; --t) {
+        const long long ctas = (long long)gx * ((mtiles + t - 1) / t) * groups;
+        const double cost = (double)((ctas + c->num_sms - 1) / c->num_sms) * (t + 0.6);
+        if (cost < best - 1e-9) {
+            best = cost;
+            tpc = t;
+        }
+    }
     dim3 grid(gx, (mtiles + tpc - 1) / tpc, groups);
     cnn::ws::conv_ws_kernel<Op><<<grid, cnn::ws::WsPlan<Op>::Threads, cnn::ws::ws_smem<Op>(), c->cur>>>(a, tpc);
     launch_check(c, "conv_ws");

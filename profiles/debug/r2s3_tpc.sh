@@ -1,0 +1,8 @@
+# A/B of the tiles-per-CTA choice: lockstep time vs active slots (C2's counts), alternated
+mkdir -p gpurun_out
+V=$PWD/profiles/debug/var
+for rep in 1 2; do
+  for lib in NEW5 NEW6; do
+    echo "== $lib"; SMX_LIB_PATH=$V/libsmx_$lib.so timeout 300 python profiles/occupancy_sweep.py --steps 30 --counts 6,10,12,48,64
+  done
+done
