@@ -35,16 +35,16 @@ sys.path.insert(0, str(ROOT / "tests"))
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 # DRAM bytes (read + write) per launch of each candidate roofline kernel (64 groups at bs 128,
 # max_batch 128) from one `ncu --set full` capture of a 64-slot lockstep
-# (profiles/r02/ncu_convs_v15.txt, profiles/debug/r2s3_ncu_all.sh)
+# (profiles/r02/ncu_convs_v17.txt, profiles/debug/r2s3_ncu_all.sh)
 TRAFFIC: dict = {
-    "K1_conv2_fwd": 1_084_283_000 + 542_001_000,
-    "K3_conv2_wgrad": 1_613_928_000 + 70_167_000,
-    "K2_conv2_dgrad": 587_626_000 + 1_015_939_000,
-    "K2_conv3_dgrad": 346_514_000 + 487_264_000,
-    "K1_conv3_fwd": 575_331_000 + 28_835_000,
-    "K3_conv3_wgrad": 845_850_000 + 70_262_000,
-    "K1_conv1_fwd": 13_078_000 + 1_014_505_000,
-    "K3_conv1_wgrad": 1_083_643_000 + 11_760_000,
+    "K1_conv2_fwd": 1_084_483_000 + 506_878_000,
+    "K3_conv2_wgrad": 1_613_938_000 + 70_397_000,
+    "K2_conv2_dgrad": 587_761_000 + 1_019_161_000,
+    "K2_conv3_dgrad": 364_734_000 + 491_350_000,
+    "K1_conv3_fwd": 575_465_000 + 29_468_000,
+    "K3_conv3_wgrad": 851_218_000 + 69_658_000,
+    "K1_conv1_fwd": 12_789_000 + 1_047_297_000,
+    "K3_conv1_wgrad": 1_084_710_000 + 9_852_000,
 }
 # what each candidate is (tensor-core mode, per launch = 64 groups at bs 128)
 KERNEL_DESC: dict = {
