@@ -321,6 +321,9 @@ cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
     return a;
 }
 
+#ifndef SMX_TPC_FILL
+#define SMX_TPC_FILL 1.5  // per-CTA pipeline fill / drain in tiles (conv_tc grid choice; profiles/debug/r2s3_tpc.sh)
+#endif
 // tiles per CTA of each tensor-core conv (amortises the CTA prologue over several M tiles)
 template <class Op>
 constexpr int conv_tpc() {
@@ -341,7 +344,7 @@ template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
     configure_ws<Op>(c);
     // tiles per CTA (one CTA per SM at a time): the count <= the Op's maximum that minimises
-    // waves x (tiles + per-CTA fill / drain ~0.6 tile), so that the last wave is not a short one
+    // waves x (tiles + per-CTA fill / drain ~1.5 tiles), so that the last wave is not a short one
     // at any slot count (e.g. 10 slots of the conv2 input gradient: 8 tiles per CTA = 2.2 waves,
     // 6 = 2.9).  It changes only the work split, never the arithmetic.
     const int mtiles = (m_max + tc3::kBM - 1) / tc3::kBM;
@@ -349,7 +352,7 @@ void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) 
     double best = 1e30;
     for (int t = conv_tpc<Op>(); t >= 1; --t) {
         const long long ctas = (long long)gx * ((mtiles + t - 1) / t) * groups;
-        const double cost = (double)((ctas + c->num_sms - 1) / c->num_sms) * (t + 0.6);
+        const double cost = (double)((ctas + c->num_sms - 1) / c->num_sms) * (t + SMX_TPC_FILL);
         if (cost < best - 1e-9) {
             best = cost;
             tpc = t;
