@@ -324,6 +324,12 @@ cnn::ConvArgs cnn_args(smx_ctx* c, const int* d_slots) {
 #ifndef SMX_TPC_FILL
 #define SMX_TPC_FILL 1.5  // per-CTA pipeline fill / drain in tiles (conv_tc grid choice; profiles/debug/r2s3_tpc.sh)
 #endif
+#ifndef SMX_TPC_FWD3
+#define SMX_TPC_FWD3 16
+#endif
+#ifndef SMX_TPC_DGR3
+#define SMX_TPC_DGR3 16
+#endif
 // tiles per CTA of each tensor-core conv (amortises the CTA prologue over several M tiles)
 template <class Op>
 constexpr int conv_tpc() {
@@ -334,11 +340,11 @@ constexpr int conv_tpc<cnn::ctc::Fwd<1>>() { return 8; }
 template <>
 constexpr int conv_tpc<cnn::ctc::Fwd<2>>() { return 16; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return 4; }
+constexpr int conv_tpc<cnn::ctc::Fwd<3>>() { return SMX_TPC_FWD3; }
 template <>
 constexpr int conv_tpc<cnn::ctc::Dgrad<2>>() { return 16; }
 template <>
-constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return 8; }
+constexpr int conv_tpc<cnn::ctc::Dgrad<3>>() { return SMX_TPC_DGR3; }
 
 template <class Op>
 void conv_tc(smx_ctx* c, const cnn::ConvArgs& a, int gx, int m_max, int groups) {
