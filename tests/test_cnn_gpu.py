@@ -90,13 +90,13 @@ def rel(a, b):
     return np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30)
 
 
-def check_first_step(ds, bs, maxb=MAXB, chan_bound=2e-5):
+def check_first_step(ds, bs, maxb=MAXB, chan_bound=2e-5, n_val=N_VAL):
     """One tensor-core step at batch size bs (mu = 0: m_1 = the gradient) against the fp32 oracle's
     loss and a float64 torch gradient."""
     _, _, off = ol.cnn_layout()
     hp = np.tile(np.float32([1.0, 0.0, 0.0, bs]), (4, 1))
     with ex.Executor(n_slots=4, n_ckpts=2, gemm_mode=ex.GEMM_TC, max_steps=64, max_batch=maxb, n_train=N_TRAIN,
-                     n_val=N_VAL, model=ex.MODEL_CNN) as e:
+                     n_val=n_val, model=ex.MODEL_CNN) as e:
         e.slot_init(0)
         e.hp_upload(0, 0, hp)
         e.train([0], 1)
@@ -132,6 +132,14 @@ def test_tc_first_step_gradient(ds, bs):
     # bs 1 / 5 / 37: batch sizes that are not multiples of the conv1 weight-gradient work item
     # (4 samples) and of the 8 image-row chunks, and batches smaller than one item
     check_first_step(ds, bs)
+
+
+@pytest.mark.parametrize("bs", [37, 1])
+def test_tc_first_step_gradient_odd_max_batch(bs):
+    # max_batch 37 (n_val a multiple of it and of 128): the conv3 input gradient's last M tile holds one
+    # sample, and at bs 37 its second TMA output box sample (37) is past max_batch, so the tensor
+    # store is clipped (kTmD2)
+    check_first_step(ol.cnn_dataset(N_TRAIN, 128 * 37, 37), bs, maxb=37, n_val=128 * 37)
 
 
 @pytest.mark.parametrize("bs", [200, 256])
