@@ -1085,14 +1085,36 @@ __global__ void __launch_bounds__(128) wgrad_reduce_kernel(ConvArgs p) {
     const int co = blockIdx.x;
     const int nsplit = (v.bs * G::OH * G::OH + kSplitRows - 1) / kSplitRows;
     const float* part = v.act + (L == 1 ? p.al.p1 : L == 2 ? p.al.p2 : p.al.p3) + (long long)co * P::Ld;
-    for (int k = threadIdx.x; k < P::Rows; k += blockDim.x) {
-        float s = 0.0f;
-        for (int i = 0; i < nsplit; ++i) s = __fadd_rn(s, part[(long long)i * G::Co * P::Ld + k]);
-        const long long at = k < 9 * G::Ci ? G::OffW + (long long)co * 9 * G::Ci + k : G::OffB + co;
-        if (p.fuse_update)
-            sgd_apply(w, m, at, s, h);
-        else
-            g[at] = s;
+    // all of the thread's elements at once (parameter / momentum loads issued first, then split by
+    // split), each summed over the splits in ascending order
+    constexpr int KI = (P::Rows + 127) / 128;
+    static_assert(KI <= 8, "elements per thread");
+    float s[KI], wv[KI], mv[KI];
+    long long at[KI];
+#pragma unroll
+    for (int j = 0; j < KI; ++j) {
+        const int k = threadIdx.x + 128 * j;
+        at[j] = k >= P::Rows ? -1 : k < 9 * G::Ci ? G::OffW + (long long)co * 9 * G::Ci + k : G::OffB + co;
+        s[j] = 0.0f;
+        if (p.fuse_update && at[j] >= 0) {
+            wv[j] = w[at[j]];
+            mv[j] = m[at[j]];
+        }
+    }
+    for (int i = 0; i < nsplit; ++i)
+#pragma unroll
+        for (int j = 0; j < KI; ++j)
+            if (at[j] >= 0) s[j] = __fadd_rn(s[j], part[(long long)i * G::Co * P::Ld + threadIdx.x + 128 * j]);
+#pragma unroll
+    for (int j = 0; j < KI; ++j) {
+        if (at[j] < 0) continue;
+        if (p.fuse_update) {  // sgd_apply on the preloaded values
+            const float mn = __fmaf_rn(h.mu, mv[j], __fmaf_rn(h.wd, wv[j], s[j]));
+            m[at[j]] = mn;
+            w[at[j]] = __fmaf_rn(h.nlr, mn, wv[j]);
+        } else {
+            g[at[j]] = s[j];
+        }
     }
 }
 
