@@ -692,7 +692,8 @@ struct Dgrad {
     // cover only those columns (conv_ws ColRanges): 9 of the 16 class x neighbour blocks are issued.
     static constexpr bool kColRanges = true;
     static __host__ __device__ constexpr int cls_at(int pos) { return (L == 2 && pos >= 2) ? (pos ^ 1) : pos; }
-    __device__ __forceinline__ void chunk_cols(int k0, int& off, int& n) const {
+    __device__ __forceinline__ void chunk_cols(int k0, int& off, int& n) const { chunk_cols_at(col0, k0, off, n); }
+    __host__ __device__ static void chunk_cols_at(int col0, int k0, int& off, int& n) {
         const int nb = k0 / G::Co, da = nb >> 1, db = nb & 1;
         constexpr int P = WImg<L>::DgrNTile / G::Ci;  // class positions per N tile
         int lo = P, hi = -1;
@@ -993,6 +994,13 @@ __device__ __forceinline__ void weight_image_body(const ConvArgs& p, int bx, int
             const int rem = uu % (WImg<L>::DgrChunks * 8 * NT);
             const int c = rem / (8 * NT), kq = (rem / NT) % 8, r = rem % NT;
             nt = NT;
+            // rows outside the chunk's column range are never read (the MMAs of a K chunk cover only
+            // the classes its neighbour feeds, conv_ws ColRanges): not written
+            {
+                int off, n;
+                ctc::Dgrad<(L >= 2 ? L : 2)>::chunk_cols_at(half * NT, ctc::Dgrad<(L >= 2 ? L : 2)>::chunk_k0(c), off, n);
+                if (r < off || r >= off + n) continue;
+            }
             const int cc = half * NT + r, cls = ctc::Dgrad<(L >= 2 ? L : 2)>::cls_at(cc / G::Ci), ci = cc % G::Ci;
             const int pi = cls >> 1, pj = cls & 1;
 #pragma unroll
