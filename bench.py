@@ -113,6 +113,11 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+# SMX_BENCH_SHARED_GPU=1: exercise the N > 1 path (rank placement, barriers, max-over-ranks
+# timing) with every rank on one GPU and gloo reductions -- a test of the code path, not a number
+SHARED_GPU = os.environ.get("SMX_BENCH_SHARED_GPU") == "1"
+
+
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -121,8 +126,13 @@ def dist_init():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:  # test mode: all ranks on the box's GPU(s), gloo for the timing reductions
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -139,7 +149,7 @@ def reduce_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -150,7 +160,7 @@ def reduce_sum(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
